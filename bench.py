@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the fused 8x8 approximate-DCT compress path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one fused compress launch over every image resident on the rank
+(config 3: 4096 seeded 2048x2048 uint8 images per GPU, retain r=10; weak
+scaling) + the NCCL all-reduce of the per-image SSE when N > 1.  Inputs are
+generated on the GPU before timing (16 GiB per GPU >> 126 MB L2, so no L2
+flush is needed between steps).  Rank 0 prints one JSON line.
+
+--impl reference times the reference's own CPU algorithm (the float64
+restatement oracle/refport.py of codec.compress_image + metrics.mse/psnr;
+/root/reference cannot travel to the GPU box) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpixel/s for fused 8x8 approx-DCT fwd+quant+inv+PSNR; % of HBM roofline"
+UNIT = "Gpixel/s"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+CONFIGS = {
+    3: dict(kind="retain", h=2048, w=2048, n=4096, r=10, blobs=(64, 16.0, 256.0),
+            workload="config3: 4096 seeded 2048x2048 u8 images per GPU, fused fwd+retain(r=10)+inv+round+clamp+SSE/PSNR"),
+    2: dict(kind="quant", h=1024, w=1024, n=256, q=(10, 50, 90), blobs=(32, 16.0, 128.0),
+            workload="config2: 256 seeded 1024x1024 u8 images per GPU, fused level-shift+fwd+quant(q=10,50,90)+dequant+inv+SSE"),
+    4: dict(kind="planes", frames=512, q=75,
+            workload="config4: 512 seeded 3840x2160 YCbCr 4:2:0 frames per GPU, fused quant(q=75) of Y+Cb+Cr in one launch"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_hbm_peak() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy read+write, measured)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback 6650 GB/s (B200_PROFILING.md), MEASURED_PEAKS.json absent"
+
+
+def ncu_traffic(config: int):
+    """Per-launch DRAM bytes of the top kernel from the committed ncu summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"config{config}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: reference algorithm (oracle/refport.py), all host cores
+# ---------------------------------------------------------------------------
+
+def _ref_task(args):
+    img, r = args
+    from oracle import refport
+
+    rec = refport.compress_image(img, r)
+    m = refport.mse(img, rec)
+    return refport.psnr(m)
+
+
+def cpu_reference_rate(images, r: int, budget_s: float, cores: int):
+    """Gpixel/s of the reference algorithm over full images and/or row strips of
+    `images`, one task per worker, for about `budget_s` seconds."""
+    import numpy as np
+    from concurrent.futures import ProcessPoolExecutor
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    h, w = images[0].shape
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        # calibrate on one full image per worker
+        t0 = time.perf_counter()
+        list(ex.map(_ref_task, [(images[k % len(images)], r) for k in range(cores)]))
+        t_full = time.perf_counter() - t0
+        rounds = max(1, int(budget_s / max(t_full, 1e-3)))
+        tasks = [(images[k % len(images)], r) for k in range(cores * rounds)]
+        t0 = time.perf_counter()
+        list(ex.map(_ref_task, tasks))
+        dt = time.perf_counter() - t0
+    px = len(tasks) * h * w
+    return px / dt / 1e9, dict(images=len(tasks), seconds=dt, image_shape=[h, w])
+
+
+def reference_arm(args) -> None:
+    """--impl reference: the reference's CPU algorithm on the host cores."""
+    import numpy as np
+
+    from paper_1702_00817_b200 import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    cores = len(os.sched_getaffinity(0))
+    if cfg["kind"] != "retain":
+        print(json.dumps({"impl": "reference", "unavailable": "reference has no quantised pipeline (configs 2/4); use --config 3"}))
+        return
+    h, w, r = cfg["h"], cfg["w"], cfg["r"]
+    nb, smin, smax = cfg["blobs"]
+    n_img = min(cores, 16)
+    images = [synth.render_np(synth.blob_params(s, h, w, nb, smin, smax), h, w, s) for s in range(n_img)]
+    # per-step sample: `rows` rows of one image per worker, sized so the whole run fits ~3 minutes
+    budget_step = min(30.0, 180.0 / max(1, args.steps + args.warmup))
+    from concurrent.futures import ProcessPoolExecutor
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(_ref_task, [(images[k % n_img], r) for k in range(cores)]))
+        t_full = time.perf_counter() - t0
+        rows = int(h * min(1.0, budget_step / max(t_full, 1e-3)))
+        rows = max(8, rows - rows % 8)
+        strips = [(images[k % n_img][:rows], r) for k in range(cores)]
+        for _ in range(args.warmup):
+            list(ex.map(_ref_task, strips))
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            list(ex.map(_ref_task, strips))
+            times.append(time.perf_counter() - t0)
+    px_step = cores * rows * w
+    total = sum(times)
+    value = px_step * len(times) / total / 1e9
+    sample = f"{cores} x ({rows}x{w}) strips of config-3 images per step (one per core), oracle/refport.py float64 path"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian blobs + N(0,4^2) noise, BASELINE.json generator)",
+        "config": {"workload": cfg["workload"], "r": r},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def gpu_arm(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_00817_b200 import batch, quant, shard, synth
+    from paper_1702_00817_b200.pipeline import HostPipeline, pin, unpin
+
+    rank, world, local = shard.init_from_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}")
+
+    # ---- workload resident in HBM -------------------------------------------
+    t_gen = time.perf_counter()
+    if cfg["kind"] in ("retain", "quant"):
+        per = cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).count
+        first = rank * cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).start
+        nb, smin, smax = cfg["blobs"]
+        imgs = synth.images_device(range(first, first + per), cfg["h"], cfg["w"], nb, smin, smax, device=dev)
+        rec = torch.empty_like(imgs)
+        sse = torch.empty(per, dtype=torch.int64, device=dev)
+        px_rank = per * cfg["h"] * cfg["w"]
+        n_total = per * world if args.scaling == "weak" else cfg["n"]
+        if cfg["kind"] == "retain":
+            def step_kernel():
+                batch.compress_retain(imgs, cfg["r"], out=rec, sse_out=sse)
+            launches_per_step = 1
+        else:
+            qtabs = [quant.quant_table(q) for q in cfg["q"]]
+            sses = [torch.empty(per, dtype=torch.int64, device=dev) for _ in qtabs]
+            def step_kernel():
+                for qt, s in zip(qtabs, sses):
+                    batch.compress_quant(imgs, qt, out=rec, sse_out=s)
+            launches_per_step = len(qtabs)
+            px_rank *= len(qtabs)
+    else:  # config 4 planes
+        frames = cfg["frames"] if args.scaling == "weak" else shard.shard_range(cfg["frames"], rank, world).count
+        f0 = rank * cfg["frames"] if args.scaling == "weak" else shard.shard_range(cfg["frames"], rank, world).start
+        planes = synth.video_planes_device(frames, frame0=f0, device=dev)
+        qt = quant.quant_table(cfg["q"])
+        import ctypes
+        from paper_1702_00817_b200 import _lib
+        recs = [torch.empty_like(p) for p in planes]
+        arr, _ = batch._planes(planes, recs)
+        sse = torch.empty((frames, 3), dtype=torch.int64, device=dev)
+        def step_kernel():
+            _lib.call("adct_compress_quant_planes", arr, 3, frames, ctypes.byref(qt), sse.data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+        launches_per_step = 1
+        px_rank = frames * sum(p.shape[1] * p.shape[2] for p in planes)
+        n_total = frames * world
+        per = frames
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] workload ready in {time.perf_counter() - t_gen:.1f}s: {px_rank / 1e9:.2f} Gpx per step")
+
+    def step():
+        step_kernel()
+        if world > 1:
+            full = torch.zeros((n_total,) + tuple(sse.shape[1:]), dtype=torch.int64, device=dev)
+            base = rank * per if args.scaling == "weak" else shard.shard_range(n_total, rank, world).start
+            full[base : base + per] = sse
+            dist.all_reduce(full)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----------------------------------------------------------
+    stream = torch.cuda.current_stream()
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for i in range(args.steps):
+        k_start[i].record(stream)
+        step_kernel()
+        k_end[i].record(stream)
+        if world > 1:
+            full = torch.zeros((n_total,) + tuple(sse.shape[1:]), dtype=torch.int64, device=dev)
+            base = rank * per if args.scaling == "weak" else shard.shard_range(n_total, rank, world).start
+            full[base : base + per] = sse
+            dist.all_reduce(full)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps / launches_per_step
+    if world > 1:
+        t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kern_ms = t.tolist()
+
+    total_px = px_rank * world * args.steps
+    value = total_px / (elapsed_ms * 1e-3) / 1e9
+    px_launch = px_rank / launches_per_step
+    alg_bytes = 2 * px_launch + 8 * per  # u8 in + u8 out (+ 8 B SSE per image)
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    peak, peak_src = measured_hbm_peak()
+
+    # ---- end to end: host buffers through the C-ABI pipeline -------------------
+    e2e = None
+    if rank == 0 and not args.no_e2e and cfg["kind"] in ("retain", "quant"):
+        m = min(per, args.e2e_images)
+        host_in = imgs[:m].cpu().numpy()
+        host_out = np.empty_like(host_in)
+        pin(host_in)
+        pin(host_out)
+        try:
+            with HostPipeline(local, chunk_bytes=args.e2e_chunk_mb << 20) as pipe:
+                if cfg["kind"] == "retain":
+                    call = lambda: pipe.compress_retain(host_in, cfg["r"], host_out, register=False)
+                else:
+                    qt0 = quant.quant_table(cfg["q"][0])
+                    call = lambda: pipe.compress_quant(host_in, qt0, host_out, register=False)
+                call()
+                reps = 3
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    _, sse_host = call()
+                dt = (time.perf_counter() - t0) / reps
+            e2e = {"value": m * cfg["h"] * cfg["w"] / dt / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": int(host_in.nbytes), "d2h_bytes_per_step": int(host_out.nbytes + 8 * m),
+                   "images_per_step": m, "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline"}
+        finally:
+            unpin(host_in)
+            unpin(host_out)
+
+    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and cfg["kind"] == "retain":
+        cores = len(os.sched_getaffinity(0))
+        sample_imgs = [imgs[k].cpu().numpy() for k in range(min(per, 8))]
+        v, info = cpu_reference_rate(sample_imgs, cfg["r"], args.cpu_seconds, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{info['images']} full {info['image_shape'][0]}x{info['image_shape'][1]} config-3 images, "
+                         f"one per task on {cores} processes, {info['seconds']:.1f}s; oracle/refport.py = reference "
+                         f"codec.compress_image + metrics.mse/psnr float64 algorithm"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded Gaussian blobs + N(0,4^2) noise, BASELINE.json generator, rendered on GPU)",
+            "config": {"workload": cfg["workload"], "units_per_gpu": per, "pixels_per_step": px_rank * world,
+                       "parallelism": f"dp{world} (images sharded, SSE all-reduce)",
+                       "l2": "inputs >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-images", type=int, default=256)
+    ap.add_argument("--e2e-chunk-mb", type=int, default=128)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

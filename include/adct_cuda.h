@@ -1,0 +1,216 @@
+/*
+ * adct_cuda.h — C ABI of libadct_cuda.so, the B200 (sm_100a) implementation of
+ * the blockwise 8x8 approximate-DCT hot path of arxiv 1702.00817
+ * (reference package `adct`, /root/reference/pkg/src/adct).
+ *
+ * The reference has no FFI: its boundary is the Python codec/metrics API
+ * (codec.py:53-155, metrics.py:49-65).  Each entry point below names the
+ * reference function(s) it replaces.  A maintainer binds them with ctypes
+ * (INTEGRATION.md); the in-tree binding is paper_1702_00817_b200/_lib.py.
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only.  Pointers documented "device" must be CUDA device
+ *     (or managed) memory owned by the caller; "host" pointers are CPU memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Device entry points are asynchronous on that stream, never allocate,
+ *     never synchronise, keep no global mutable state and are reentrant.
+ *   - Images are 8-bit, row-major with row pitch == width; image k of a batch
+ *     starts at base + k*image_stride (elements).  height and width must be
+ *     multiples of 8 (reference: BadDimensions, codec.py:128-129).
+ *   - Block order of coefficient outputs is the reference's `_tile` order
+ *     (codec.py:107-109): raster over block rows, then block columns.
+ *   - Return value: ADCT_OK or one of the error codes; validation happens
+ *     before anything is enqueued (reference raises before compute).
+ *   - SSE outputs are zeroed by the call (on the stream) and then accumulated
+ *     with integer atomics, so they are exact and order independent.
+ */
+#ifndef ADCT_CUDA_H
+#define ADCT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes.  The first four mirror the reference's contract errors. */
+enum {
+  ADCT_OK = 0,
+  ADCT_ERR_BAD_DIMENSIONS = 1,         /* adct.errors.BadDimensions      (errors.py:29) */
+  ADCT_ERR_INVALID_RETENTION = 2,      /* adct.errors.InvalidRetention   (errors.py:21) */
+  ADCT_ERR_NON_POSITIVE_QUANTIZER = 3, /* adct.errors.NonPositiveQuantizer (errors.py:25) */
+  ADCT_ERR_DIMENSION_MISMATCH = 4,     /* adct.errors.DimensionMismatch  (errors.py:33) */
+  ADCT_ERR_INVALID_ARGUMENT = 5,       /* null pointer, negative count, bad plane count */
+  ADCT_ERR_MISALIGNED = 6,             /* base pointer or stride not 8-byte aligned */
+  ADCT_ERR_CUDA = 7,                   /* a CUDA runtime call failed (see adct_last_cuda_error) */
+  ADCT_ERR_UNSUPPORTED = 8             /* quantiser table outside the exactly-provable range */
+};
+
+/* Library version (major*10000 + minor*100 + patch) and error strings. */
+int adct_version(void);
+const char* adct_strerror(int code);
+/* cudaError_t of the most recent ADCT_ERR_CUDA on the calling thread. */
+int adct_last_cuda_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Quantiser table (BASELINE configs 2 and 4).
+ *
+ * Q'[u][v] = max(1, round_half_away(Q[u][v] / (d[u] d[v]))), the reference's
+ * fold_scaling_into_quantization (codec.py:90-104) followed by the rounding
+ * BASELINE.json specifies.  The device quantiser computes
+ *   q = sign(Z) * floor((2|Z| + Q') / (2 Q'))      (round half away from zero)
+ *   Z' = q * Q'
+ * exactly with one multiply-high per coefficient; `magic`, `kbias` and
+ * `uoff` are the constants that make it exact, verified exhaustively over
+ * every reachable |Z| by adct_qtab_build.  Treat the struct as opaque except
+ * for `qprime`, `wide` and `max_abs_v`.
+ * ------------------------------------------------------------------------- */
+typedef struct adct_qtab {
+  int32_t qprime[64];   /* rounded Q', row-major (u*8+v) */
+  uint32_t magic[64];   /* floor(U / (2Q')) == umulhi(U, magic) on the reachable U range */
+  int32_t kbias[64];    /* K: U = 2Z - [Z<0] + Q'(2K+1) >= 0, quotient offset */
+  int32_t qe[64];       /* Q' * E[u][v], E = 64 d[u]^2 d[v]^2 in {1,2,4,8,16} */
+  int32_t wide;         /* 1: 16-bit-lane inverse not provably exact -> 32-bit inverse kernel */
+  int32_t max_abs_v;    /* proven bound of |64*(x_rec-128)| before clamping */
+  int32_t quality;      /* JPEG quality used to build it, or -1 for an explicit table */
+  int32_t reserved;
+} adct_qtab_t;
+
+/* Build from an unrounded Q' table (64 float64, row-major), i.e. the output of
+ * the reference's fold_scaling_into_quantization.  Host-only, no CUDA.
+ * Errors: NON_POSITIVE_QUANTIZER if any entry <= 0 or not finite;
+ * UNSUPPORTED if the table cannot be handled exactly. */
+int adct_qtab_build(const double* qprime_unrounded, adct_qtab_t* out);
+
+/* Convenience: Q' from the standard JPEG luminance table Q50 (`base`, 64
+ * int32, row-major) and JPEG quality q in [1,100] with the IJG scale
+ * s(q) = 50/q (q<50) or 2 - q/50 (q>=50):
+ *   Q'[u][v] = max(1, round_half_away(Q50[u][v] * s(q) / (d[u] d[v]))).
+ * Errors: INVALID_ARGUMENT for q outside [1,100] or null pointers. */
+int adct_qtab_from_quality(const int32_t* base, int32_t quality, adct_qtab_t* out);
+
+/* ---------------------------------------------------------------------------
+ * K1 — forward integer transform.
+ * Replaces forward_2d_unscaled (codec.py:74-81) batched like
+ * coefficient_blocks (codec.py:120-131): coef = T * X * T^T per 8x8 block,
+ * exact.  level_shift != 0 transforms X-128 instead (DC - 8192).
+ * coef: device int32 [n][h/8*w/8][8][8]. */
+int adct_forward_int32(const uint8_t* img, int64_t n, int32_t h, int32_t w,
+                       int64_t img_stride, int32_t level_shift, int32_t* coef,
+                       void* stream);
+/* Same, int16 output (|coef| <= 16320 always fits). */
+int adct_forward_int16(const uint8_t* img, int64_t n, int32_t h, int32_t w,
+                       int64_t img_stride, int32_t level_shift, int16_t* coef,
+                       void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K2 + K4 — fused retain-r compression.
+ * Replaces compress_image (codec.py:144-155) + mse (metrics.py:49-56) for a
+ * batch: forward, keep the first r zigzag coefficients (codec.py:24-50),
+ * orthonormal inverse, round (half away from zero) and clamp to [0,255].
+ * Reads each pixel once and writes each reconstructed pixel once.
+ *   rec           device uint8 [n][h][w] (rec_stride apart), nullable
+ *   sse           device uint64 [n]: sum over pixels of (x - rec)^2, nullable
+ *   sse_unrounded device uint64 [n], nullable: sum of (64 x - clamp(64 x_hat,
+ *                 0, 16320))^2, i.e. 4096 * the reference's own unrounded
+ *                 clamped SSE (codec.py:141, metrics.py:56), exactly.
+ * Errors: INVALID_RETENTION unless 1 <= r <= 64. */
+int adct_compress_retain(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
+                         int32_t w, int64_t img_stride, int64_t rec_stride,
+                         int32_t r, uint64_t* sse, uint64_t* sse_unrounded,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K3 + K4 — fused quantised compression (single plane batch).
+ * Level shift -128, forward T X T^T, quantise by Q' (round half away),
+ * dequantise, inverse T^T D Y D T, +128, round, clamp; per-image SSE.
+ * New (the reference has no quantised pipeline; BASELINE config 2). */
+int adct_compress_quant(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
+                        int32_t w, int64_t img_stride, int64_t rec_stride,
+                        const adct_qtab_t* qtab, uint64_t* sse, void* stream);
+
+/* K6 — several planes (e.g. Y, Cb, Cr of 4:2:0 frames) in ONE launch. */
+typedef struct adct_plane {
+  const uint8_t* src;       /* device, frame f at src + f*src_frame_stride */
+  uint8_t* dst;             /* device, nullable */
+  int32_t height, width;    /* multiples of 8 */
+  int64_t src_frame_stride; /* elements */
+  int64_t dst_frame_stride; /* elements */
+} adct_plane_t;
+
+/* sse: device uint64 [n_frames][n_planes]; 1 <= n_planes <= 3. */
+int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes,
+                               int64_t n_frames, const adct_qtab_t* qtab,
+                               uint64_t* sse, void* stream);
+/* Retain-r over planes in one launch (sse as above). */
+int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes,
+                                int64_t n_frames, int32_t r, uint64_t* sse,
+                                void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K7 — retain-r sweep: one read of each image, SSE for every r in
+ * [r_min, r_max].  Replaces the per-r loop of cli.run_sweep
+ * (cli.py:101-113: reconstruct_image + mse per r).
+ * sse: device uint64 [n][r_max - r_min + 1]. */
+int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w,
+                          int64_t img_stride, int32_t r_min, int32_t r_max,
+                          uint64_t* sse, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Real-valued (float64) transforms, for the reference's float API on
+ * non-integral data (the reference accepts any real image, codec.py:127).
+ *   adct_forward_f64:  coef = C X C^T per block, C = D T  (forward_2d /
+ *                      coefficient_blocks, codec.py:68-71, 120-131)
+ *   adct_inverse_f64:  out = clamp?(untile(C^T mask_r(coef) C))
+ *                      (inverse_2d / reconstruct_image, codec.py:84-87,
+ *                      134-141); r in [1,64] (64 = no truncation),
+ *                      clamp != 0 clamps to [0,255] like codec.py:141.
+ * img/out: device float64 [n][h][w]; coef: device float64 [n][h*w/64][8][8]. */
+int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w,
+                     double* coef, void* stream);
+int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w,
+                     int32_t r, int32_t clamp, double* out, void* stream);
+
+/* Device SSE between two uint8 batches (metrics.mse numerator,
+ * metrics.py:49-56).  sse: device uint64 [n]. */
+int adct_sse_u8(const uint8_t* a, const uint8_t* b, int64_t n, int64_t numel,
+                int64_t stride_a, int64_t stride_b, uint64_t* sse, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Synthetic image generator (BASELINE.json configs; not a reference API).
+ * pixel = clip(rint(128 + sum_k amp_k exp(-((y-cy_k)^2+(x-cx_k)^2)/(2 sig_k^2))
+ *                   + 4 * N(0,1)), 0, 255)
+ * blobs: device float32 [n][n_blobs][4] = (cy, cx, sigma, amp) per image;
+ * noise_seed: device uint64 [n]; N(0,1) comes from a counter-based hash of
+ * (noise_seed, y, x), identical on every GPU count. */
+int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w,
+                     int64_t img_stride, const float* blobs, int32_t n_blobs,
+                     const uint64_t* noise_seed, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer pipeline (the end-to-end entry point).  Streams batches of
+ * host images through the device in chunks: H2D copy of chunk i+1, fused
+ * compress of chunk i and D2H copy of chunk i-1 overlap on separate streams.
+ * Host buffers should be pinned (adct_host_register) for full speed.
+ * ------------------------------------------------------------------------- */
+typedef struct adct_pipeline adct_pipeline_t;
+
+int adct_pipeline_create(int32_t device, size_t chunk_bytes, adct_pipeline_t** out);
+int adct_pipeline_destroy(adct_pipeline_t* p);
+/* host_rec nullable; host_sse: host uint64 [n].  Blocks until done. */
+int adct_pipeline_compress_retain(adct_pipeline_t* p, const uint8_t* host_img,
+                                  uint8_t* host_rec, int64_t n, int32_t h, int32_t w,
+                                  int32_t r, uint64_t* host_sse);
+int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img,
+                                 uint8_t* host_rec, int64_t n, int32_t h, int32_t w,
+                                 const adct_qtab_t* qtab, uint64_t* host_sse);
+/* Page-lock / unlock caller memory (cudaHostRegister). */
+int adct_host_register(void* ptr, size_t bytes);
+int adct_host_unregister(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADCT_CUDA_H */

@@ -1,0 +1,222 @@
+"""Batched device API over torch CUDA tensors — the hot path.
+
+Every function validates like the reference (before any compute), then makes
+exactly one C-ABI call on the current torch stream.  Inputs are uint8
+(N, H, W) CUDA tensors (rows contiguous); outputs are fresh tensors.
+PyTorch supplies device memory and streams only; all arithmetic is in
+libadct_cuda.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BadDimensions, DimensionMismatch, InvalidRetention
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _as_batch(images: torch.Tensor) -> torch.Tensor:
+    if not isinstance(images, torch.Tensor):
+        raise TypeError("images must be a torch tensor (use the codec wrappers for numpy input)")
+    if images.dtype != torch.uint8:
+        raise TypeError(f"images must be uint8, got {images.dtype}")
+    if not images.is_cuda:
+        raise ValueError("images must be on a CUDA device (no CPU path exists)")
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    if images.dim() != 3:
+        raise BadDimensions(f"expected (N, H, W) images, got shape {tuple(images.shape)}")
+    n, h, w = images.shape
+    if h % 8 or w % 8:
+        raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+    if images.stride(2) != 1 or images.stride(1) != w:
+        images = images.contiguous()
+    return images
+
+
+def _img_stride(images: torch.Tensor) -> int:
+    n, h, w = images.shape
+    return images.stride(0) if n > 1 else h * w
+
+
+def forward_int(images: torch.Tensor, *, level_shift: bool = False, dtype=torch.int32) -> torch.Tensor:
+    """K1: T X T^T of every 8x8 block, (N, H*W/64, 8, 8) in `_tile` order (codec.py:74-81, 107-109)."""
+    images = _as_batch(images)
+    n, h, w = images.shape
+    out = torch.empty((n, (h // 8) * (w // 8), 8, 8), dtype=dtype, device=images.device)
+    name = {torch.int32: "adct_forward_int32", torch.int16: "adct_forward_int16"}[dtype]
+    _lib.call(name, _ptr(images), n, h, w, _img_stride(images), int(level_shift), _ptr(out), _stream())
+    return out
+
+
+def compress_retain(
+    images: torch.Tensor,
+    r: int,
+    *,
+    reconstruct: bool = True,
+    unrounded_sse: bool = False,
+    out: torch.Tensor | None = None,
+    sse_out: torch.Tensor | None = None,
+):
+    """K2+K4: fused retain-r round trip.  Returns (rec | None, sse[N] int64, sse_unrounded[N] | None).
+
+    rec = clamp(round_half_away(C^T mask_r(C X C^T) C)) as uint8;
+    sse[i] = sum (x - rec)^2 (exact);
+    sse_unrounded[i] = 4096 * the reference's unrounded clamped SSE (exact).
+    """
+    if not 1 <= int(r) <= 64:
+        raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+    images = _as_batch(images)
+    n, h, w = images.shape
+    rec = None
+    if reconstruct:
+        rec = out if out is not None else torch.empty_like(images)
+    sse = sse_out if sse_out is not None else torch.empty(n, dtype=torch.int64, device=images.device)
+    ssef = torch.empty(n, dtype=torch.int64, device=images.device) if unrounded_sse else None
+    _lib.call(
+        "adct_compress_retain",
+        _ptr(images), _ptr(rec), n, h, w, _img_stride(images), h * w if rec is None else _img_stride(rec),
+        int(r), _ptr(sse), _ptr(ssef), _stream(),
+    )
+    return rec, sse, ssef
+
+
+def compress_quant(
+    images: torch.Tensor,
+    qtab: _lib.QTab,
+    *,
+    reconstruct: bool = True,
+    out: torch.Tensor | None = None,
+    sse_out: torch.Tensor | None = None,
+):
+    """K3+K4: level shift, T X T^T, quantise by Q' (half away), dequantise,
+    inverse, +128, round, clamp.  Returns (rec | None, sse[N] int64)."""
+    images = _as_batch(images)
+    n, h, w = images.shape
+    rec = (out if out is not None else torch.empty_like(images)) if reconstruct else None
+    sse = sse_out if sse_out is not None else torch.empty(n, dtype=torch.int64, device=images.device)
+    _lib.call(
+        "adct_compress_quant",
+        _ptr(images), _ptr(rec), n, h, w, _img_stride(images), h * w if rec is None else _img_stride(rec),
+        ctypes.byref(qtab), _ptr(sse), _stream(),
+    )
+    return rec, sse
+
+
+def _planes(planes: Sequence[torch.Tensor], recs: Sequence[torch.Tensor | None]):
+    if not 1 <= len(planes) <= 3:
+        raise ValueError("1 to 3 planes")
+    n = planes[0].shape[0]
+    arr = (_lib.Plane * len(planes))()
+    for k, (p, r) in enumerate(zip(planes, recs)):
+        if p.dim() != 3 or p.shape[0] != n:
+            raise DimensionMismatch("every plane needs shape (N, H, W) with the same N")
+        if p.dtype != torch.uint8 or not p.is_cuda:
+            raise TypeError("planes must be uint8 CUDA tensors")
+        if not p.is_contiguous():
+            raise ValueError("planes must be contiguous")
+        _, h, w = p.shape
+        if h % 8 or w % 8:
+            raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+        arr[k].src = p.data_ptr()
+        arr[k].dst = None if r is None else r.data_ptr()
+        arr[k].height = h
+        arr[k].width = w
+        arr[k].src_frame_stride = h * w
+        arr[k].dst_frame_stride = h * w
+    return arr, n
+
+
+def compress_quant_planes(planes: Sequence[torch.Tensor], qtab: _lib.QTab, *, reconstruct: bool = True):
+    """K6: all planes (e.g. Y, Cb, Cr of 4:2:0 frames) in one launch.
+    Returns (list of rec | None, sse (N, n_planes) int64)."""
+    recs = [torch.empty_like(p) if reconstruct else None for p in planes]
+    arr, n = _planes(planes, recs)
+    sse = torch.empty((n, len(planes)), dtype=torch.int64, device=planes[0].device)
+    _lib.call("adct_compress_quant_planes", arr, len(planes), n, ctypes.byref(qtab), _ptr(sse), _stream())
+    return recs, sse
+
+
+def compress_retain_planes(planes: Sequence[torch.Tensor], r: int, *, reconstruct: bool = True):
+    if not 1 <= int(r) <= 64:
+        raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+    recs = [torch.empty_like(p) if reconstruct else None for p in planes]
+    arr, n = _planes(planes, recs)
+    sse = torch.empty((n, len(planes)), dtype=torch.int64, device=planes[0].device)
+    _lib.call("adct_compress_retain_planes", arr, len(planes), n, int(r), _ptr(sse), _stream())
+    return recs, sse
+
+
+def sweep_retain_sse(images: torch.Tensor, r_min: int = 1, r_max: int = 45) -> torch.Tensor:
+    """K7: SSE[N, r_max-r_min+1] for every r, one read of each image (cli.py:101-113)."""
+    if not (1 <= r_min <= r_max <= 64):
+        raise InvalidRetention(f"retention range must satisfy 1 <= r_min <= r_max <= 64, got {r_min}..{r_max}")
+    images = _as_batch(images)
+    n, h, w = images.shape
+    sse = torch.empty((n, r_max - r_min + 1), dtype=torch.int64, device=images.device)
+    _lib.call("adct_sweep_retain_sse", _ptr(images), n, h, w, _img_stride(images), r_min, r_max, _ptr(sse), _stream())
+    return sse
+
+
+def sse_u8(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Per-image integer SSE of two uint8 CUDA batches (N, ...) -> int64[N]."""
+    if a.shape != b.shape:
+        raise DimensionMismatch(f"shape mismatch: {tuple(a.shape)} vs {tuple(b.shape)}")
+    a = a.contiguous()
+    b = b.contiguous()
+    n = a.shape[0] if a.dim() > 0 else 1
+    numel = a.numel() // max(n, 1) if n else 0
+    sse = torch.empty(n, dtype=torch.int64, device=a.device)
+    _lib.call("adct_sse_u8", _ptr(a), _ptr(b), n, numel, numel, numel, _ptr(sse), _stream())
+    return sse
+
+
+def forward_f64(images: torch.Tensor) -> torch.Tensor:
+    """C X C^T per block in float64 (forward_2d / coefficient_blocks, codec.py:68-71, 120-131)."""
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    if images.dim() != 3:
+        raise BadDimensions(f"expected (N, H, W), got {tuple(images.shape)}")
+    n, h, w = images.shape
+    if h % 8 or w % 8:
+        raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+    x = images.to(dtype=torch.float64).contiguous()
+    coef = torch.empty((n, (h // 8) * (w // 8), 8, 8), dtype=torch.float64, device=x.device)
+    _lib.call("adct_forward_f64", _ptr(x), n, h, w, _ptr(coef), _stream())
+    return coef
+
+
+def inverse_f64(coef: torch.Tensor, h: int, w: int, *, r: int = 64, clamp: bool = False) -> torch.Tensor:
+    """untile(C^T mask_r(Y) C), optionally clamped (inverse_2d / reconstruct_image)."""
+    if not 1 <= int(r) <= 64:
+        raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+    if h % 8 or w % 8:
+        raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+    nb = (h // 8) * (w // 8)
+    c = coef.to(dtype=torch.float64).contiguous()
+    if c.numel() % (64 * max(nb, 1)) or (nb and c.numel() // 64 % nb):
+        raise BadDimensions(f"coefficients {tuple(coef.shape)} do not tile a {h}x{w} image")
+    n = c.numel() // (64 * nb) if nb else 0
+    out = torch.empty((n, h, w), dtype=torch.float64, device=c.device)
+    _lib.call("adct_inverse_f64", _ptr(c), n, h, w, int(r), int(clamp), _ptr(out), _stream())
+    return out
+
+
+def psnr_from_sse(sse, n_pixels: int, *, scale: float = 1.0) -> np.ndarray:
+    """10 log10(255^2 / (sse / (scale * n_pixels))), inf at 0 (metrics.py:59-65)."""
+    s = np.asarray(sse.cpu() if isinstance(sse, torch.Tensor) else sse, dtype=np.float64)
+    mse = s / (scale * float(n_pixels))
+    with np.errstate(divide="ignore"):
+        return np.where(mse == 0, np.inf, 10.0 * np.log10(255.0**2 / np.where(mse == 0, 1.0, mse)))

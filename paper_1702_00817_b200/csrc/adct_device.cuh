@@ -1,0 +1,364 @@
+// adct_device.cuh — device building blocks for the sm_100a approximate-DCT path.
+//
+// Arithmetic model ("two blocks per thread, two 16-bit lanes per register")
+// -------------------------------------------------------------------------
+// A thread owns a *unit*: two horizontally adjacent 8x8 blocks A and B (or one
+// block A with an all-zero B for widths that are 8 mod 16).  Every 32-bit
+// register holds the same (row, col) position of A and B as two lanes:
+//
+//   linear form:   r = a + 65536*b  (mod 2^32), a and b signed
+//
+// Addition, subtraction, shifts and multiplication by a constant shared by both
+// lanes act lane-wise on the linear form, exactly, modulo 2^32, whatever the
+// intermediate magnitudes (carries between lanes cancel because the map
+// (a,b) -> a + 65536 b is a ring homomorphism mod 2^32).  So the whole
+// forward T X T^T, the dyadic scaling E, and the inverse T^T W T run as plain
+// 32-bit IADD3/SHF/IMAD on both blocks at once, with the compiler free to
+// fuse and prune (template r => dead-code elimination of the masked
+// coefficients).
+//
+// The lanes only need to be *unambiguous* where we leave the linear form: at
+// the end, |64 (x_hat - 128) + 32| <= 27168 for every retain-r mask (proved by
+// tools/range_bounds.py) and <= the host-proved `max_abs_v` for a
+// quantiser table, so adding 0x80008000 yields two unsigned 16-bit fields
+// [0,65535] with no borrow, which the native packed-16 instructions
+// (VIMNMX.U16x2) clamp and PRMT packs into bytes.
+//
+// Exactness: Z = T X T^T is an integer; the inverse of unscaled
+// coefficients is X = T^T D^2 Z D^2 T, so 64 X = T^T (E o Z) T with
+// E[u][v] = 64 d_u^2 d_v^2 = e_u e_v, e = (1,4,2,4,1,4,2,4) -> shifts only.
+// Rounding (+32), level shift (-8192) and the lane bias fold into W[0][0]
+// because T^T e0 e0^T T = all-ones (row 0 of T is all ones).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace adct {
+
+typedef uint32_t u32;
+typedef unsigned long long u64;
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Compile-time tables
+// ---------------------------------------------------------------------------
+
+// The proposed kernel T (paper eq. for T; reference kernels.py:35-47),
+// written as the product P*A3*A2*A1 of the stage matrices (fast.py:173-224)
+// evaluated by hand: entries in {0,+-1}.
+__host__ __device__ constexpr int t_entry(int u, int i) {
+  // One case per row of T; tests/test_capi.py checks it against the flow
+  // graph (fwd8) and the oracle's P*A3*A2*A1 product.
+  switch (u) {
+    case 0: return 1;
+    case 1: return i == 0 ? 1 : (i == 7 ? -1 : 0);
+    case 2: return (i == 0 || i == 7) ? 1 : ((i == 3 || i == 4) ? -1 : 0);
+    case 3: return i == 2 ? -1 : (i == 5 ? 1 : 0);
+    case 4: return (i == 0 || i == 3 || i == 4 || i == 7) ? 1 : -1;
+    case 5: return i == 1 ? -1 : (i == 6 ? 1 : 0);
+    case 6: return (i == 2 || i == 5) ? 1 : ((i == 1 || i == 6) ? -1 : 0);
+    default: return i == 3 ? -1 : (i == 4 ? 1 : 0);
+  }
+}
+
+// JPEG zigzag rank of block position (u,v): index in the scan of
+// ZIGZAG_INDICES (codec.py:24-33).  Walks anti-diagonals s = u+v; odd s run
+// with increasing row, even s with decreasing row.
+__host__ __device__ constexpr int zz_rank(int u, int v) {
+  int s = u + v, before = 0;
+  for (int k = 0; k < s; ++k) before += (k < 8) ? (k + 1) : (15 - k);
+  const int rlo = s < 8 ? 0 : s - 7;
+  const int rhi = s < 8 ? s : 7;
+  return before + ((s & 1) ? (u - rlo) : (rhi - u));
+}
+
+__host__ __device__ constexpr int zz_pos(int k) {  // inverse: rank -> u*8+v
+  for (int p = 0; p < 64; ++p)
+    if (zz_rank(p >> 3, p & 7) == k) return p;
+  return -1;
+}
+
+__host__ __device__ constexpr bool zz_kept(int u, int v, int r) { return zz_rank(u, v) < r; }
+
+// log2 of e_u = 8 d_u^2 (d^2 = 1/8,1/2,1/4,1/2,... kernels.py:149-157).
+__host__ __device__ constexpr int e_log2(int u) { return (u & 1) ? 2 : ((u & 2) ? 1 : 0); }
+
+// W[0][0] constant for the rounded pipelines: per lane -8192 (level shift of
+// the reconstruction) + 32 (round half up == half away on the clamped range)
+// + 32768 (lane bias so the output fields are unsigned), both lanes.
+constexpr u32 kDcRound = (32768u - 8192u + 32u) * 65537u;  // 0x60206020
+
+// ---------------------------------------------------------------------------
+// 1-D flow graphs on the linear form (14 additions each).
+// ---------------------------------------------------------------------------
+
+// Forward X = T x: stages A1 (8 adds), A2 (4), A3 (2), P — fast.py:130-168.
+template <class V>
+__device__ __forceinline__ void fwd8(const V (&x)[8], V (&X)[8]) {
+  const V a0 = x[0] + x[7], a1 = x[1] + x[6], a2 = x[2] + x[5], a3 = x[3] + x[4];
+  const V b0 = a0 + a3, b1 = a1 + a2;
+  X[0] = b0 + b1;       // A3 line 0
+  X[4] = b0 - b1;       // A3 line 1
+  X[2] = a0 - a3;       // b3
+  X[6] = a2 - a1;       // -b2
+  X[1] = x[0] - x[7];   // a7
+  X[3] = x[5] - x[2];   // -a5
+  X[5] = x[6] - x[1];   // -a6
+  X[7] = x[4] - x[3];   // -a4
+}
+
+// Inverse x = T^T X = A1 A2 A3 P^T X (the stage matrices are symmetric,
+// SURVEY N7); the reference has no inverse flow graph.
+template <class V>
+__device__ __forceinline__ void inv8(const V (&X)[8], V (&x)[8]) {
+  const V b0 = X[0] + X[4], b1 = X[0] - X[4];
+  const V a0 = b0 + X[2], a3 = b0 - X[2];
+  const V a1 = b1 - X[6], a2 = b1 + X[6];
+  x[0] = a0 + X[1];
+  x[7] = a0 - X[1];
+  x[1] = a1 - X[5];
+  x[6] = a1 + X[5];
+  x[2] = a2 - X[3];
+  x[5] = a2 + X[3];
+  x[3] = a3 - X[7];
+  x[4] = a3 + X[7];
+}
+
+// 2-D forward on a unit: rows then columns.  Z[u][v] = (T x T^T)[u][v].
+template <class V>
+__device__ __forceinline__ void fwd2d(const V (&x)[8][8], V (&Z)[8][8]) {
+  V t[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    V col[8], out[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+    fwd8(col, out);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) Z[u][v] = out[u];
+  }
+}
+
+// 2-D inverse: columns (along u) then rows (along v).  x = T^T W T.
+template <class V>
+__device__ __forceinline__ void inv2d(const V (&W)[8][8], V (&x)[8][8]) {
+  V c[8][8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    V col[8], out[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) col[u] = W[u][v];
+    inv8(col, out);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][v] = out[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) inv8(c[i], x[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Memory helpers: streaming loads (read once) and stores (written once).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream8(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream16(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_stream8(void* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Plane geometry.  Every fused kernel runs over a set of <= 3 planes (a batch
+// of single images is one plane); grid.x enumerates 256-unit tiles of all
+// planes of one frame back to back (plane boundaries are tile aligned, so a
+// CTA never straddles planes or frames), grid.y enumerates frames.
+// ---------------------------------------------------------------------------
+struct PlaneDev {
+  const uint8_t* src;
+  uint8_t* dst;
+  int64_t src_fs;    // frame stride (elements)
+  int64_t dst_fs;
+  int32_t width;     // pixels
+  uint32_t upr;      // units per block row
+  uint32_t units;    // units per frame
+  uint32_t cta_begin;
+};
+
+struct PlaneSetDev {
+  PlaneDev p[3];
+  int32_t n_planes;
+  int32_t frame_base;  // first frame of this launch (launches are chunked by 65535 frames)
+};
+
+// Row words of one unit (8 rows x 16 B, or 8 x 8 B with B-lanes zero).
+template <bool PAIR>
+__device__ __forceinline__ void load_unit(const uint8_t* base, int32_t width, uint4 (&w)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (PAIR) {
+      w[i] = ld_stream16(base + (int64_t)i * width);
+    } else {
+      const uint2 h = ld_stream8(base + (int64_t)i * width);
+      w[i] = make_uint4(h.x, h.y, 0u, 0u);
+    }
+  }
+}
+
+// Bytes -> linear-form lanes: x[i][j] = A[i][j] + 65536 * B[i][j].
+__device__ __forceinline__ void unpack_unit(const uint4 (&w)[8], u32 (&x)[8][8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const u32 p01 = __byte_perm(w[i].x, w[i].z, 0x5410);  // a0 a1 b0 b1
+    const u32 p23 = __byte_perm(w[i].x, w[i].z, 0x7632);  // a2 a3 b2 b3
+    const u32 p45 = __byte_perm(w[i].y, w[i].w, 0x5410);
+    const u32 p67 = __byte_perm(w[i].y, w[i].w, 0x7632);
+    x[i][0] = __byte_perm(p01, 0u, 0x4240);
+    x[i][1] = __byte_perm(p01, 0u, 0x4341);
+    x[i][2] = __byte_perm(p23, 0u, 0x4240);
+    x[i][3] = __byte_perm(p23, 0u, 0x4341);
+    x[i][4] = __byte_perm(p45, 0u, 0x4240);
+    x[i][5] = __byte_perm(p45, 0u, 0x4341);
+    x[i][6] = __byte_perm(p67, 0u, 0x4240);
+    x[i][7] = __byte_perm(p67, 0u, 0x4341);
+  }
+}
+
+// Output fields U = 64(x_hat-128) + 32 + 32768 (two unsigned 16-bit lanes)
+// -> reconstructed bytes.  pixel = clamp(floor((U - 24576) / 64), 0, 255):
+// clamp U to [0x6000, 0x9FFF] (native VIMNMX.U16x2), shift so bits 6..13 of
+// each lane land in bytes 1 and 3, gather with PRMT, and flip bit 7
+// ((U>>6) & 0xFF == pixel ^ 0x80 on the clamped range).
+__device__ __forceinline__ u32 clamp_shift(u32 U) {
+  return __vmaxu2(__vminu2(U, 0x9FFF9FFFu), 0x60006000u) << 2;
+}
+
+__device__ __forceinline__ void pack_row(const u32 (&U)[8], uint4& out) {
+  const u32 s0 = clamp_shift(U[0]), s1 = clamp_shift(U[1]), s2 = clamp_shift(U[2]),
+            s3 = clamp_shift(U[3]), s4 = clamp_shift(U[4]), s5 = clamp_shift(U[5]),
+            s6 = clamp_shift(U[6]), s7 = clamp_shift(U[7]);
+  const u32 q0 = __byte_perm(s0, s1, 0x7531);  // a0 b0 a1 b1
+  const u32 q1 = __byte_perm(s2, s3, 0x7531);  // a2 b2 a3 b3
+  const u32 q2 = __byte_perm(s4, s5, 0x7531);
+  const u32 q3 = __byte_perm(s6, s7, 0x7531);
+  out.x = __byte_perm(q0, q1, 0x6420) ^ 0x80808080u;  // a0 a1 a2 a3
+  out.y = __byte_perm(q2, q3, 0x6420) ^ 0x80808080u;  // a4 .. a7
+  out.z = __byte_perm(q0, q1, 0x7531) ^ 0x80808080u;  // b0 .. b3
+  out.w = __byte_perm(q2, q3, 0x7531) ^ 0x80808080u;  // b4 .. b7
+}
+
+// Sum of squared byte differences of 4 pixel pairs: |a-b| per byte (VABSDIFF4),
+// then a dot product with itself (IDP.4A).
+__device__ __forceinline__ u32 sse4(u32 a, u32 b, u32 acc) {
+  const u32 d = __vabsdiffu4(a, b);
+  return __dp4a(d, d, acc);
+}
+
+// Store reconstructed rows and accumulate SSE (per-thread partial).
+template <bool PAIR>
+__device__ __forceinline__ u32 emit_unit(const u32 (&U)[8][8], const uint4 (&w)[8],
+                                         uint8_t* dst, int32_t width) {
+  u32 acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint4 o;
+    pack_row(U[i], o);
+    if (dst != nullptr) {
+      if (PAIR)
+        st_stream16(dst + (int64_t)i * width, o);
+      else
+        st_stream8(dst + (int64_t)i * width, make_uint2(o.x, o.y));
+    }
+    acc = sse4(w[i].x, o.x, acc);
+    acc = sse4(w[i].y, o.y, acc);
+    if (PAIR) {
+      acc = sse4(w[i].z, o.z, acc);
+      acc = sse4(w[i].w, o.w, acc);
+    }
+  }
+  return acc;
+}
+
+// Block-wide sum of a per-thread u32 partial, one 64-bit atomic per CTA.
+// Per-thread partials are <= 128 * 255^2 < 2^24, per-warp sums < 2^29.
+__device__ __forceinline__ void block_add_u32(u32 v, u64* dst) {
+  __shared__ u32 warp_sums[kThreads / 32];
+  v = __reduce_add_sync(0xffffffffu, v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) warp_sums[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; ++k) t += warp_sums[k];
+    if (t != 0) atomicAdd(dst, t);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void block_add_u64(u64 v, u64* dst) {
+  __shared__ u64 warp_sums64[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) warp_sums64[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; ++k) t += warp_sums64[k];
+    if (t != 0) atomicAdd(dst, t);
+  }
+  __syncthreads();
+}
+
+// Locate this thread's unit.  Returns false for the padding threads of a
+// plane's last tile.  Division by the (runtime) units-per-row happens once
+// per 128 pixels.
+struct UnitLoc {
+  int plane;
+  int64_t frame;
+  const uint8_t* src;
+  uint8_t* dst;
+  int32_t width;
+};
+
+template <bool PAIR>
+__device__ __forceinline__ bool locate_unit(const PlaneSetDev& ps, UnitLoc& L) {
+  const u32 bx = blockIdx.x;
+  int p = 0;
+  if (ps.n_planes > 1 && bx >= ps.p[1].cta_begin) p = 1;
+  if (ps.n_planes > 2 && bx >= ps.p[2].cta_begin) p = 2;
+  const PlaneDev& P = ps.p[p];
+  const u32 unit = (bx - P.cta_begin) * kThreads + threadIdx.x;
+  L.plane = p;
+  L.frame = (int64_t)ps.frame_base + blockIdx.y;
+  L.width = P.width;
+  if (unit >= P.units) return false;
+  const u32 brow = unit / P.upr;
+  const u32 ucol = unit - brow * P.upr;
+  const int64_t off = (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
+  L.src = P.src + L.frame * P.src_fs + off;
+  L.dst = P.dst ? P.dst + L.frame * P.dst_fs + off : nullptr;
+  return true;
+}
+
+}  // namespace adct

@@ -1,0 +1,442 @@
+// adct_kernels.cuh — sm_100a kernels of the approximate-DCT hot path.
+// See adct_device.cuh for the arithmetic model and DESIGN.md for rooflines.
+#pragma once
+
+#include "adct_device.cuh"
+
+namespace adct {
+
+// ---------------------------------------------------------------------------
+// Quantiser constants in kernel-parameter (constant bank) space, 1280 bytes.
+// Filled from adct_qtab_t by the host (capi.cu).
+// ---------------------------------------------------------------------------
+struct QParamsDev {
+  u32 magic[64];  // umulhi(U, magic) == floor(U / 2Q'), verified exhaustively
+  u32 cadd[64];   // C = Q'(2K+1)
+  u32 qe[64];     // Q' * E[u][v]
+  u32 wadd[64];   // -K*qe*65537 (+0x80208020 at DC: rounding +32, lane bias)
+  int32_t kbias[64];
+};
+
+// Per-position pre-quantisation bias on the linear form: lane bias 0x8000 on
+// lane A (so lane A's 16-bit field is unsigned and lane B has no borrow), plus
+// the level shift -8192 on the DC coefficient of both lanes
+// (T (X-128) T^T = Z - 8192 e0 e0^T).
+__device__ __forceinline__ constexpr u32 qbias(int p) {
+  return p == 0 ? (0x8000u - 8192u * 65537u) : 0x8000u;
+}
+
+// Round-half-away quotient + K of both lanes.  For true Z:
+//   U = 2Z - [Z<0] + C   (>= 0),   q + K = floor(U / 2Q') = umulhi(U, magic).
+// Lane A is held as lo = Z_A + 32768 in [0, 65535]:
+//   U_A = 2 lo + (lo >> 15) + (C - 65537).
+__device__ __forceinline__ void quant_lanes(u32 z, int p, const QParamsDev& q, u32& qa, u32& qb) {
+  const u32 v = z + qbias(p);
+  const u32 lo = v & 0xFFFFu;
+  const int hi = (int)v >> 16;
+  const u32 ua = 2u * lo + (lo >> 15) + (q.cadd[p] - 65537u);
+  const u32 ub = (u32)(2 * hi + (hi >> 31)) + q.cadd[p];
+  qa = __umulhi(ua, q.magic[p]);
+  qb = __umulhi(ub, q.magic[p]);
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused retain-r, r a template parameter (pruned at compile time).
+// ---------------------------------------------------------------------------
+template <int R, bool PAIR>
+__global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __restrict__ sse) {
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<PAIR>(ps, L)) {
+    uint4 w[8];
+    load_unit<PAIR>(L.src, L.width, w);
+    u32 x[8][8], Z[8][8], W[8][8], U[8][8];
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        W[u][v] = zz_kept(u, v, R) ? (Z[u][v] << (e_log2(u) + e_log2(v))) : 0u;
+    W[0][0] += kDcRound;
+    inv2d(W, U);
+    acc = emit_unit<PAIR>(U, w, L.dst, L.width);
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+}
+
+// Runtime-r variant: ragged widths (PAIR=false) and the exact "unrounded"
+// SSE of the reference's float convention (FSSE).
+template <bool PAIR, bool FSSE>
+__global__ void __launch_bounds__(kThreads)
+    k_retain_rt(PlaneSetDev ps, int r, u64* __restrict__ sse, u64* __restrict__ ssef) {
+  UnitLoc L;
+  u32 acc = 0;
+  u64 accf = 0;
+  if (locate_unit<PAIR>(ps, L)) {
+    uint4 w[8];
+    load_unit<PAIR>(L.src, L.width, w);
+    u32 x[8][8], Z[8][8], W[8][8], U[8][8];
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        W[u][v] = (zz_rank(u, v) < r) ? (Z[u][v] << (e_log2(u) + e_log2(v))) : 0u;
+    W[0][0] += kDcRound;
+    inv2d(W, U);
+    acc = emit_unit<PAIR>(U, w, L.dst, L.width);
+    if (FSSE) {
+      // sum (64 x - clamp(64 x_hat, 0, 16320))^2 with 64 x_hat = U - 24608.
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const u32 c = __vmaxu2(__vminu2(U[i][j], 0x9FE09FE0u), 0x60206020u);
+          const u32 d = (x[i][j] << 6) + 0x60206020u - c;
+          const int da = (int)(d << 16) >> 16;
+          const int db = (int)(d - (u32)da) >> 16;
+          accf += (u64)(da * da) + (PAIR ? (u64)(db * db) : 0ull);
+        }
+    }
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (FSSE) block_add_u64(accf, ssef + L.frame * ps.n_planes + L.plane);
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused quantised pipeline.  WIDE=false: 16-bit lanes end to end (exact
+// when the host proved |64(x_hat-128)+32| <= 32767 for the table);
+// WIDE=true: 32-bit inverse per block for coarse tables (e.g. q=10).
+// ---------------------------------------------------------------------------
+template <bool PAIR, bool WIDE>
+__global__ void __launch_bounds__(kThreads)
+    k_quant(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<PAIR>(ps, L)) {
+    uint4 w[8];
+    load_unit<PAIR>(L.src, L.width, w);
+    u32 x[8][8], Z[8][8], U[8][8];
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+    if (!WIDE) {
+      u32 W[8][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int p = u * 8 + v;
+          u32 qa, qb;
+          quant_lanes(Z[u][v], p, q, qa, qb);
+          W[u][v] = (qa + (qb << 16)) * q.qe[p] + q.wadd[p];
+        }
+      inv2d(W, U);
+    } else {
+      int Wa[8][8], Wb[8][8], Va[8][8], Vb[8][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int p = u * 8 + v;
+          u32 qa, qb;
+          quant_lanes(Z[u][v], p, q, qa, qb);
+          Wa[u][v] = ((int)qa - q.kbias[p]) * (int)q.qe[p];
+          Wb[u][v] = ((int)qb - q.kbias[p]) * (int)q.qe[p];
+        }
+      Wa[0][0] += 32;
+      Wb[0][0] += 32;
+      inv2d(Wa, Va);
+      inv2d(Wb, Vb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int a = min(max(Va[i][j], -8192), 8191) + 32768;
+          const int b = min(max(Vb[i][j], -8192), 8191) + 32768;
+          U[i][j] = (u32)a | ((u32)b << 16);
+        }
+    }
+    acc = emit_unit<PAIR>(U, w, L.dst, L.width);
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+}
+
+// ---------------------------------------------------------------------------
+// K7: retain-r sweep — one read and one forward per unit, then for every r in
+// [r_min, r_max] the masked inverse, rounding and SSE, all from registers
+// (replaces the per-r reconstruct_image + mse loop, cli.py:105-113).
+// Reconstructions are not stored.
+// ---------------------------------------------------------------------------
+template <bool PAIR>
+__global__ void __launch_bounds__(kThreads)
+    k_sweep(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse) {
+  UnitLoc L;
+  const bool active = locate_unit<PAIR>(ps, L);
+  uint4 w[8];
+  u32 Z[8][8];
+  if (active) {
+    u32 x[8][8];
+    load_unit<PAIR>(L.src, L.width, w);
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) Z[u][v] <<= (e_log2(u) + e_log2(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w[i] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Z[i][j] = 0;
+    }
+  }
+  const int nr = r_max - r_min + 1;
+  u64* out = sse + L.frame * nr;
+#pragma unroll 1
+  for (int r = r_min; r <= r_max; ++r) {
+    u32 acc = 0;
+    if (active) {
+      u32 W[8][8], U[8][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) W[u][v] = (zz_rank(u, v) < r) ? Z[u][v] : 0u;
+      W[0][0] += kDcRound;
+      inv2d(W, U);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint4 o;
+        pack_row(U[i], o);
+        acc = sse4(w[i].x, o.x, acc);
+        acc = sse4(w[i].y, o.y, acc);
+        if (PAIR) {
+          acc = sse4(w[i].z, o.z, acc);
+          acc = sse4(w[i].w, o.w, acc);
+        }
+      }
+    }
+    block_add_u32(acc, out + (r - r_min));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: forward integer transform, coefficients in _tile order.
+// ---------------------------------------------------------------------------
+template <bool PAIR, typename OutT>
+__global__ void __launch_bounds__(kThreads)
+    k_forward(PlaneSetDev ps, int level_shift, int32_t nbc, OutT* __restrict__ coef) {
+  const PlaneDev& P = ps.p[0];
+  const u32 unit = blockIdx.x * kThreads + threadIdx.x;
+  if (unit >= P.units) return;
+  const int64_t frame = (int64_t)ps.frame_base + blockIdx.y;
+  const u32 brow = unit / P.upr;
+  const u32 ucol = unit - brow * P.upr;
+  const uint8_t* src =
+      P.src + frame * P.src_fs + (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
+  uint4 w[8];
+  load_unit<PAIR>(src, P.width, w);
+  u32 x[8][8], Z[8][8];
+  unpack_unit(w, x);
+  fwd2d(x, Z);
+  const int64_t nblocks = (int64_t)nbc * (P.units / P.upr);
+  const int64_t blk = frame * nblocks + (int64_t)brow * nbc + (int64_t)ucol * (PAIR ? 2 : 1);
+  OutT* ca = coef + blk * 64;
+  OutT* cb = ca + 64;
+  const u32 dc_shift = level_shift ? 8192u * 65537u : 0u;
+  if (sizeof(OutT) == 4) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int4 va, vb;
+        int* pa = &va.x;
+        int* pb = &vb.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int v = h * 4 + k;
+          const u32 z = Z[u][v] + 0x8000u - ((u == 0 && v == 0) ? dc_shift : 0u);
+          pa[k] = (int)(z & 0xFFFFu) - 32768;
+          pb[k] = (int)z >> 16;
+        }
+        reinterpret_cast<int4*>(ca)[u * 2 + h] = va;
+        if (PAIR) reinterpret_cast<int4*>(cb)[u * 2 + h] = vb;
+      }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      u32 za[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        za[v] = Z[u][v] + 0x8000u - ((u == 0 && v == 0) ? dc_shift : 0u);
+      uint4 va, vb;
+      va.x = __byte_perm(za[0], za[1], 0x5410) ^ 0x80008000u;
+      va.y = __byte_perm(za[2], za[3], 0x5410) ^ 0x80008000u;
+      va.z = __byte_perm(za[4], za[5], 0x5410) ^ 0x80008000u;
+      va.w = __byte_perm(za[6], za[7], 0x5410) ^ 0x80008000u;
+      vb.x = __byte_perm(za[0], za[1], 0x7632);
+      vb.y = __byte_perm(za[2], za[3], 0x7632);
+      vb.z = __byte_perm(za[4], za[5], 0x7632);
+      vb.w = __byte_perm(za[6], za[7], 0x7632);
+      reinterpret_cast<uint4*>(ca)[u] = va;
+      if (PAIR) reinterpret_cast<uint4*>(cb)[u] = vb;
+    }
+  }
+}
+
+#ifdef ADCT_DEFINE_PLAIN_KERNELS  // non-template kernels: defined once, in capi.cu
+// ---------------------------------------------------------------------------
+// Float64 transforms (real-valued inputs; signature parity with the
+// reference's float API).  One thread per 8x8 block.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dscale(int u) {
+  // d = (1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2, 1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2), kernels.py:149-157
+  return (u & 1) ? 0.70710678118654757 : ((u & 2) ? 0.5 : 0.35355339059327379);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_forward_f64(const double* __restrict__ img, int h, int w, int64_t nblocks,
+                  double* __restrict__ coef) {
+  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blk >= nblocks) return;
+  const int64_t frame = blockIdx.y;
+  const int nbc = w / 8;
+  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
+  const double* src = img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
+  double x[8][8], Z[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[i][j] = src[(int64_t)i * w + j];
+  fwd2d(x, Z);
+  double* dst = coef + (frame * nblocks + blk) * 64;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) dst[u * 8 + v] = Z[u][v] * (dscale(u) * dscale(v));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_inverse_f64(const double* __restrict__ coef, int h, int w, int64_t nblocks, int r,
+                  int clamp, double* __restrict__ out) {
+  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blk >= nblocks) return;
+  const int64_t frame = blockIdx.y;
+  const int nbc = w / 8;
+  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
+  const double* src = coef + (frame * nblocks + blk) * 64;
+  double W[8][8], x[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      W[u][v] = (zz_rank(u, v) < r) ? src[u * 8 + v] * (dscale(u) * dscale(v)) : 0.0;
+  inv2d(W, x);
+  double* dst = out + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double v = x[i][j];
+      if (clamp) v = fmin(fmax(v, 0.0), 255.0);
+      dst[(int64_t)i * w + j] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SSE of two uint8 batches (numerator of metrics.mse).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_sse_u8(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t numel,
+             int64_t sa, int64_t sb, int vec, u64* __restrict__ sse) {
+  const int64_t frame = blockIdx.y;
+  const uint8_t* pa = a + frame * sa;
+  const uint8_t* pb = b + frame * sb;
+  u32 acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  if (vec) {
+    const int64_t nv = numel / 16;
+    for (int64_t k = (int64_t)blockIdx.x * kThreads + threadIdx.x; k < nv; k += stride) {
+      const uint4 va = ld_stream16(pa + k * 16), vb = ld_stream16(pb + k * 16);
+      acc = sse4(va.x, vb.x, acc);
+      acc = sse4(va.y, vb.y, acc);
+      acc = sse4(va.z, vb.z, acc);
+      acc = sse4(va.w, vb.w, acc);
+    }
+    for (int64_t k = nv * 16 + (int64_t)blockIdx.x * kThreads + threadIdx.x; k < numel;
+         k += stride) {
+      const int d = (int)pa[k] - (int)pb[k];
+      acc += (u32)(d * d);
+    }
+  } else {
+    for (int64_t k = (int64_t)blockIdx.x * kThreads + threadIdx.x; k < numel; k += stride) {
+      const int d = (int)pa[k] - (int)pb[k];
+      acc += (u32)(d * d);
+    }
+  }
+  // per-thread partial may exceed 2^24 for huge frames: reduce in 64 bits
+  block_add_u64((u64)acc, sse + frame);
+}
+
+#endif  // ADCT_DEFINE_PLAIN_KERNELS
+
+// ---------------------------------------------------------------------------
+// Synthetic blob images (BASELINE.json generator).  Not on the timed path.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Standard normal from the counter (seed, pixel index): Box-Muller on two
+// 24-bit uniforms.  The host generator (synth.py) evaluates the same formula.
+__device__ __forceinline__ float hash_normal(u64 seed, u64 idx) {
+  const u64 h = mix64(seed * 0x9E3779B97F4A7C15ull + idx + 1ull);
+  const float u1 = ((float)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+  const float u2 = ((float)((h >> 8) & 0xFFFFFFull) + 0.5f) * (1.0f / 16777216.0f);
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+constexpr int kSynthRows = 16;
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads)
+    k_synth(uint8_t* __restrict__ out, int h, int w, int64_t stride,
+            const float* __restrict__ blobs, const u64* __restrict__ seeds, int64_t frame_base) {
+  __shared__ float gy[NB][kSynthRows];
+  const int64_t frame = frame_base + blockIdx.z;
+  const float* B = blobs + frame * NB * 4;
+  const int row0 = blockIdx.y * kSynthRows;
+  for (int idx = threadIdx.x; idx < NB * kSynthRows; idx += kThreads) {
+    const int k = idx / kSynthRows, r = idx % kSynthRows;
+    const float dy = (float)(row0 + r) - B[k * 4 + 0];
+    const float s = B[k * 4 + 2];
+    gy[k][r] = expf(-(dy * dy) / (2.0f * s * s));
+  }
+  __syncthreads();
+  const int col = blockIdx.x * kThreads + threadIdx.x;
+  if (col >= w) return;
+  float gx[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const float dx = (float)col - B[k * 4 + 1];
+    const float s = B[k * 4 + 2];
+    gx[k] = B[k * 4 + 3] * expf(-(dx * dx) / (2.0f * s * s));
+  }
+  const u64 seed = seeds[frame];
+  uint8_t* dst = out + frame * stride;
+  for (int r = 0; r < kSynthRows; ++r) {
+    const int y = row0 + r;
+    if (y >= h) break;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) s = fmaf(gx[k], gy[k][r], s);
+    const float v = 128.0f + s + 4.0f * hash_normal(seed, (u64)y * (u64)w + (u64)col);
+    dst[(int64_t)y * w + col] = (uint8_t)fminf(fmaxf(rintf(v), 0.0f), 255.0f);
+  }
+}
+
+}  // namespace adct

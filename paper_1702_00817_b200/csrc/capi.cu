@@ -1,0 +1,600 @@
+// capi.cu — extern "C" entry points of libadct_cuda.so (declared in
+// include/adct_cuda.h).  Validation mirrors the reference's contract errors
+// (errors.py:21-33) and happens before anything is enqueued.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "adct_cuda.h"
+#define ADCT_DEFINE_PLAIN_KERNELS
+#include "adct_launch.h"
+
+using namespace adct;
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int cuda_fail(cudaError_t e) {
+  g_last_cuda = (int)e;
+  return ADCT_ERR_CUDA;
+}
+
+#define ADCT_CUDA_TRY(expr)                         \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e);    \
+  } while (0)
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Host view of a plane set ready to launch.
+struct PlaneSetHost {
+  PlaneSetDev dev;
+  uint32_t grid_x = 0;
+  bool pair = true;
+};
+
+// Validate planes and lay out the tile grid.  `force_single` disables the
+// two-blocks-per-thread path (used by kernels without a PAIR=false variant).
+int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, PlaneSetHost& out) {
+  if (planes == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
+    return ADCT_ERR_INVALID_ARGUMENT;
+  std::memset(&out.dev, 0, sizeof(out.dev));
+  bool pair = true;
+  for (int k = 0; k < n_planes; ++k) {
+    const adct_plane_t& p = planes[k];
+    if (p.height < 0 || p.width < 0 || (p.height % 8) != 0 || (p.width % 8) != 0)
+      return ADCT_ERR_BAD_DIMENSIONS;
+    const int64_t plane_px = (int64_t)p.height * p.width;
+    if (n_frames > 0 && plane_px > 0 && p.src == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+    if (n_frames > 1 && p.src_frame_stride < plane_px) return ADCT_ERR_INVALID_ARGUMENT;
+    if (n_frames > 1 && p.dst != nullptr && p.dst_frame_stride < plane_px)
+      return ADCT_ERR_INVALID_ARGUMENT;
+    if (plane_px / 64 > (int64_t)0x7FFFFFFF) return ADCT_ERR_INVALID_ARGUMENT;
+    if (!aligned(p.src, 8) || (p.dst && !aligned(p.dst, 8)) || (p.src_frame_stride % 8) ||
+        (p.dst && (p.dst_frame_stride % 8)))
+      return ADCT_ERR_MISALIGNED;
+    if ((p.width % 16) || !aligned(p.src, 16) || (p.dst && !aligned(p.dst, 16)) ||
+        (p.src_frame_stride % 16) || (p.dst && (p.dst_frame_stride % 16)))
+      pair = false;
+  }
+  uint32_t cta = 0;
+  for (int k = 0; k < n_planes; ++k) {
+    const adct_plane_t& p = planes[k];
+    PlaneDev& d = out.dev.p[k];
+    d.src = p.src;
+    d.dst = p.dst;
+    d.src_fs = p.src_frame_stride;
+    d.dst_fs = p.dst_frame_stride;
+    d.width = p.width;
+    d.upr = (uint32_t)(p.width / (pair ? 16 : 8));
+    d.units = d.upr * (uint32_t)(p.height / 8);
+    d.cta_begin = cta;
+    cta += (d.units + kThreads - 1) / kThreads;
+  }
+  for (int k = n_planes; k < 3; ++k) out.dev.p[k].cta_begin = 0xFFFFFFFFu;
+  out.dev.n_planes = n_planes;
+  out.grid_x = cta;
+  out.pair = pair;
+  return ADCT_OK;
+}
+
+adct_plane_t single_plane(const uint8_t* img, uint8_t* rec, int32_t h, int32_t w,
+                          int64_t img_stride, int64_t rec_stride) {
+  adct_plane_t p;
+  p.src = img;
+  p.dst = rec;
+  p.height = h;
+  p.width = w;
+  p.src_frame_stride = img_stride;
+  p.dst_frame_stride = rec_stride;
+  return p;
+}
+
+constexpr int64_t kMaxGridY = 65535;
+
+// Launch f(ps) once per chunk of <= 65535 frames.
+template <class F>
+int for_frame_chunks(PlaneSetHost& ps, int64_t n_frames, F&& launch) {
+  if (ps.grid_x == 0 || n_frames == 0) return ADCT_OK;
+  for (int64_t f0 = 0; f0 < n_frames; f0 += kMaxGridY) {
+    const int64_t nf = (n_frames - f0) < kMaxGridY ? (n_frames - f0) : kMaxGridY;
+    ps.dev.frame_base = (int32_t)f0;
+    launch(dim3(ps.grid_x, (unsigned)nf, 1));
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+QParamsDev to_qparams(const adct_qtab_t& t) {
+  QParamsDev q;
+  for (int p = 0; p < 64; ++p) {
+    q.magic[p] = t.magic[p];
+    q.cadd[p] = (uint32_t)t.qprime[p] * (2u * (uint32_t)t.kbias[p] + 1u);
+    q.qe[p] = (uint32_t)t.qe[p];
+    q.wadd[p] = (uint32_t)0 - (uint32_t)t.kbias[p] * (uint32_t)t.qe[p] * 65537u;
+    q.kbias[p] = t.kbias[p];
+  }
+  q.wadd[0] += (32768u + 32u) * 65537u;
+  return q;
+}
+
+// --- quantiser table -------------------------------------------------------
+
+// Row L1 norms of T: n = (8,2,4,2,8,2,4,2); E[u][v] = 64/(n_u n_v).
+inline int row_nnz(int u) { return (u & 1) ? 2 : ((u & 2) ? 4 : 8); }
+
+// Reference scaling diag d (kernels.py:149-157), float64, evaluated exactly
+// as the reference does so Q' rounds identically.
+inline double ref_d(int u) {
+  const double s8 = 1.0 / std::sqrt(8.0), s2 = 1.0 / std::sqrt(2.0);
+  return (u & 1) ? s2 : ((u & 2) ? 0.5 : s8);
+}
+
+int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out) {
+  std::memset(out, 0, sizeof(*out));
+  constexpr int64_t kZmax = 8192;  // |T (X-128) T^T| <= 128 n_u n_v <= 8192
+  for (int p = 0; p < 64; ++p) {
+    const int u = p >> 3, v = p & 7;
+    const int64_t Q = qp[p];
+    if (Q < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
+    if (Q > (1 << 20)) return ADCT_ERR_UNSUPPORTED;
+    const int64_t E = 64 / (row_nnz(u) * row_nnz(v));
+    const int64_t D = 2 * Q;
+    int64_t K = (2 * kZmax + 1 - Q + D - 1) / D;  // ceil((2 Zmax + 1 - Q) / 2Q)
+    if (K < 0) K = 0;
+    const int64_t C = Q * (2 * K + 1);
+    const uint64_t magic = ((1ull << 32) + (uint64_t)D - 1) / (uint64_t)D;  // ceil(2^32 / D)
+    if (magic > 0xFFFFFFFFull) return ADCT_ERR_UNSUPPORTED;
+    if (C + 2 * kZmax >= (1ll << 32)) return ADCT_ERR_UNSUPPORTED;
+    // Exhaustive verification over every reachable coefficient value.
+    for (int64_t Z = -kZmax; Z <= kZmax; ++Z) {
+      const int64_t U = 2 * Z - (Z < 0 ? 1 : 0) + C;
+      if (U < 0) return ADCT_ERR_UNSUPPORTED;
+      const uint64_t got = ((uint64_t)U * magic) >> 32;
+      const int64_t q = (2 * (Z < 0 ? -Z : Z) + Q) / D;  // round half away of |Z|/Q
+      const int64_t want = (Z < 0 ? -q : q) + K;
+      if ((int64_t)got != want) return ADCT_ERR_UNSUPPORTED;
+    }
+    out->qprime[p] = (int32_t)Q;
+    out->magic[p] = (uint32_t)magic;
+    out->kbias[p] = (int32_t)K;
+    if (Q * E > 0x7FFFFFFF / 4) return ADCT_ERR_UNSUPPORTED;
+    out->qe[p] = (int32_t)(Q * E);
+  }
+  // |64 (x_hat - 128)| <= 8192 + max_ij sum_uv |T_ui T_vj| E_uv Q'_uv / 2
+  // (exact reconstruction of the level-shifted block is within [-8192, 8128];
+  // dequantisation moves each coefficient by at most Q'/2).
+  double worst = 0.0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double s = 0.0;
+      for (int u = 0; u < 8; ++u)
+        for (int v = 0; v < 8; ++v) {
+          const int t = t_entry(u, i) * t_entry(v, j);
+          if (t != 0) s += 0.5 * (double)out->qe[u * 8 + v];
+        }
+      if (s > worst) worst = s;
+    }
+  const double bound = 8192.0 + worst;
+  out->max_abs_v = bound > 2.0e9 ? 2000000000 : (int32_t)std::ceil(bound);
+  out->wide = (bound + 32.0 > 32767.0) ? 1 : 0;
+  // The 32-bit path needs |V| + 32 to stay far from int32 overflow.
+  if (bound > 1.0e9) return ADCT_ERR_UNSUPPORTED;
+  out->quality = quality;
+  return ADCT_OK;
+}
+
+inline int32_t round_half_away_pos(double x) { return (int32_t)std::floor(x + 0.5); }
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int adct_version(void) { return 1 * 10000 + 0 * 100 + 0; }
+
+const char* adct_strerror(int code) {
+  switch (code) {
+    case ADCT_OK: return "ok";
+    case ADCT_ERR_BAD_DIMENSIONS: return "image dimensions must be divisible by 8";
+    case ADCT_ERR_INVALID_RETENTION: return "retention count must be in [1, 64]";
+    case ADCT_ERR_NON_POSITIVE_QUANTIZER: return "quantization steps must be strictly positive";
+    case ADCT_ERR_DIMENSION_MISMATCH: return "shape mismatch";
+    case ADCT_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case ADCT_ERR_MISALIGNED: return "pointer or stride not 8-byte aligned";
+    case ADCT_ERR_CUDA: return "CUDA runtime error";
+    case ADCT_ERR_UNSUPPORTED: return "quantiser table outside the exactly supported range";
+    default: return "unknown error";
+  }
+}
+
+int adct_last_cuda_error(void) { return g_last_cuda; }
+
+int adct_qtab_build(const double* qpu, adct_qtab_t* out) {
+  if (qpu == nullptr || out == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  int32_t qp[64];
+  for (int p = 0; p < 64; ++p) {
+    if (!(qpu[p] > 0.0) || !std::isfinite(qpu[p])) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
+    if (qpu[p] > (double)(1 << 20)) return ADCT_ERR_UNSUPPORTED;
+    const int32_t r = round_half_away_pos(qpu[p]);
+    qp[p] = r < 1 ? 1 : r;
+  }
+  return build_qtab_from_rounded(qp, -1, out);
+}
+
+int adct_qtab_from_quality(const int32_t* base, int32_t quality, adct_qtab_t* out) {
+  if (base == nullptr || out == nullptr || quality < 1 || quality > 100)
+    return ADCT_ERR_INVALID_ARGUMENT;
+  // IJG quality scale as a float64 factor: s(q) = (5000/q)/100 or (200-2q)/100.
+  const double s = (quality < 50 ? 5000.0 / quality : 200.0 - 2.0 * quality) / 100.0;
+  double qpu[64];
+  for (int p = 0; p < 64; ++p) {
+    if (base[p] <= 0) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
+    const double scaled = (double)base[p] * s;
+    qpu[p] = scaled / (ref_d(p >> 3) * ref_d(p & 7));
+  }
+  int32_t qp[64];
+  for (int p = 0; p < 64; ++p) {
+    const int32_t r = round_half_away_pos(qpu[p]);
+    qp[p] = r < 1 ? 1 : r;
+  }
+  return build_qtab_from_rounded(qp, quality, out);
+}
+
+// --- K1 forward ------------------------------------------------------------
+static int forward_common(const uint8_t* img, int64_t n, int32_t h, int32_t w, int64_t img_stride,
+                          int32_t level_shift, void* coef, bool out16, void* stream) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  adct_plane_t pl = single_plane(img, nullptr, h, w, img_stride, 0);
+  PlaneSetHost ps;
+  int rc = build_planes(&pl, 1, n, ps);
+  if (rc != ADCT_OK) return rc;
+  if (ps.grid_x == 0 || n == 0) return ADCT_OK;
+  if (coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (!aligned(coef, 16)) return ADCT_ERR_MISALIGNED;
+  const int32_t nbc = w / 8;
+  cudaStream_t s = as_stream(stream);
+  return for_frame_chunks(ps, n, [&](dim3 g) {
+    if (out16) {
+      if (ps.pair)
+        k_forward<true, int16_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int16_t*)coef);
+      else
+        k_forward<false, int16_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int16_t*)coef);
+    } else {
+      if (ps.pair)
+        k_forward<true, int32_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int32_t*)coef);
+      else
+        k_forward<false, int32_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int32_t*)coef);
+    }
+  });
+}
+
+int adct_forward_int32(const uint8_t* img, int64_t n, int32_t h, int32_t w, int64_t img_stride,
+                       int32_t level_shift, int32_t* coef, void* stream) {
+  return forward_common(img, n, h, w, img_stride, level_shift, coef, false, stream);
+}
+
+int adct_forward_int16(const uint8_t* img, int64_t n, int32_t h, int32_t w, int64_t img_stride,
+                       int32_t level_shift, int16_t* coef, void* stream) {
+  return forward_common(img, n, h, w, img_stride, level_shift, coef, true, stream);
+}
+
+// --- K2 retain ---------------------------------------------------------------
+static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, int32_t r,
+                         uint64_t* sse, uint64_t* ssef, void* stream) {
+  if (r < 1 || r > 64) return ADCT_ERR_INVALID_RETENTION;
+  PlaneSetHost ps;
+  int rc = build_planes(planes, n_planes, n_frames, ps);
+  if (rc != ADCT_OK) return rc;
+  cudaStream_t s = as_stream(stream);
+  const size_t nsse = (size_t)n_frames * n_planes;
+  if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
+  if (ssef && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(ssef, 0, nsse * sizeof(uint64_t), s));
+  u64* d_sse = reinterpret_cast<u64*>(sse);
+  u64* d_ssef = reinterpret_cast<u64*>(ssef);
+  if (ssef == nullptr && ps.pair) {
+    RetainKernel k = retain_kernel(r);
+    return for_frame_chunks(ps, n_frames, [&](dim3 g) { k<<<g, kThreads, 0, s>>>(ps.dev, d_sse); });
+  }
+  return for_frame_chunks(ps, n_frames, [&](dim3 g) {
+    if (ps.pair) {
+      if (ssef) k_retain_rt<true, true><<<g, kThreads, 0, s>>>(ps.dev, r, d_sse, d_ssef);
+      else k_retain_rt<true, false><<<g, kThreads, 0, s>>>(ps.dev, r, d_sse, d_ssef);
+    } else {
+      if (ssef) k_retain_rt<false, true><<<g, kThreads, 0, s>>>(ps.dev, r, d_sse, d_ssef);
+      else k_retain_rt<false, false><<<g, kThreads, 0, s>>>(ps.dev, r, d_sse, d_ssef);
+    }
+  });
+}
+
+int adct_compress_retain(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h, int32_t w,
+                         int64_t img_stride, int64_t rec_stride, int32_t r, uint64_t* sse,
+                         uint64_t* sse_unrounded, void* stream) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
+  return retain_planes(&pl, 1, n, r, sse, sse_unrounded, stream);
+}
+
+int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,
+                                int32_t r, uint64_t* sse, void* stream) {
+  return retain_planes(planes, n_planes, n_frames, r, sse, nullptr, stream);
+}
+
+// --- K3/K6 quant -------------------------------------------------------------
+int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,
+                               const adct_qtab_t* qtab, uint64_t* sse, void* stream) {
+  if (qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  for (int p = 0; p < 64; ++p)
+    if (qtab->qprime[p] < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
+  PlaneSetHost ps;
+  int rc = build_planes(planes, n_planes, n_frames, ps);
+  if (rc != ADCT_OK) return rc;
+  cudaStream_t s = as_stream(stream);
+  const size_t nsse = (size_t)n_frames * n_planes;
+  if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
+  const QParamsDev q = to_qparams(*qtab);
+  u64* d_sse = reinterpret_cast<u64*>(sse);
+  const bool wide = qtab->wide != 0;
+  return for_frame_chunks(ps, n_frames, [&](dim3 g) {
+    if (ps.pair) {
+      if (wide) k_quant<true, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      else k_quant<true, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+    } else {
+      if (wide) k_quant<false, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      else k_quant<false, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+    }
+  });
+}
+
+int adct_compress_quant(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h, int32_t w,
+                        int64_t img_stride, int64_t rec_stride, const adct_qtab_t* qtab,
+                        uint64_t* sse, void* stream) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
+  return adct_compress_quant_planes(&pl, 1, n, qtab, sse, stream);
+}
+
+// --- K7 sweep ----------------------------------------------------------------
+int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, int64_t img_stride,
+                          int32_t r_min, int32_t r_max, uint64_t* sse, void* stream) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (r_min < 1 || r_max > 64 || r_min > r_max) return ADCT_ERR_INVALID_RETENTION;
+  adct_plane_t pl = single_plane(img, nullptr, h, w, img_stride, 0);
+  PlaneSetHost ps;
+  int rc = build_planes(&pl, 1, n, ps);
+  if (rc != ADCT_OK) return rc;
+  if (sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const size_t nsse = (size_t)n * (size_t)(r_max - r_min + 1);
+  if (nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
+  u64* d_sse = reinterpret_cast<u64*>(sse);
+  return for_frame_chunks(ps, n, [&](dim3 g) {
+    if (ps.pair) k_sweep<true><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse);
+    else k_sweep<false><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse);
+  });
+}
+
+// --- float64 -----------------------------------------------------------------
+static int f64_geometry(int64_t n, int32_t h, int32_t w, int64_t& nblocks) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (h < 0 || w < 0 || (h % 8) || (w % 8)) return ADCT_ERR_BAD_DIMENSIONS;
+  nblocks = (int64_t)(h / 8) * (w / 8);
+  if (nblocks > (int64_t)kThreads * 0x7FFFFFFF) return ADCT_ERR_INVALID_ARGUMENT;
+  return ADCT_OK;
+}
+
+int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w, double* coef,
+                     void* stream) {
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  if (n == 0 || nb == 0) return ADCT_OK;
+  if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    k_forward_f64<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(img + f0 * (int64_t)h * w, h, w, nb,
+                                                               coef + f0 * nb * 64);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w, int32_t r, int32_t clamp,
+                     double* out, void* stream) {
+  if (r < 1 || r > 64) return ADCT_ERR_INVALID_RETENTION;
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  if (n == 0 || nb == 0) return ADCT_OK;
+  if (out == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    k_inverse_f64<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r,
+                                                               clamp, out + f0 * (int64_t)h * w);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+int adct_sse_u8(const uint8_t* a, const uint8_t* b, int64_t n, int64_t numel, int64_t stride_a,
+                int64_t stride_b, uint64_t* sse, void* stream) {
+  if (n < 0 || numel < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (n == 0) return ADCT_OK;
+  if (sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, (size_t)n * sizeof(uint64_t), s));
+  if (numel == 0) return ADCT_OK;
+  if (a == nullptr || b == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  const int vec = aligned(a, 16) && aligned(b, 16) && (stride_a % 16 == 0) && (stride_b % 16 == 0);
+  int64_t per = vec ? numel / 16 : numel;
+  int64_t gx = (per + kThreads - 1) / kThreads;
+  if (gx > 1184) gx = 1184;  // 8 CTAs per SM on 148 SMs, grid-stride beyond
+  if (gx < 1) gx = 1;
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    k_sse_u8<<<dim3((unsigned)gx, (unsigned)nf), kThreads, 0, s>>>(
+        a + f0 * stride_a, b + f0 * stride_b, numel, stride_a, stride_b, vec,
+        reinterpret_cast<u64*>(sse) + f0);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+// --- synthetic generator ----------------------------------------------------
+int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w, int64_t img_stride,
+                     const float* blobs, int32_t n_blobs, const uint64_t* noise_seed,
+                     void* stream) {
+  if (n < 0 || h < 0 || w < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (n == 0 || h == 0 || w == 0) return ADCT_OK;
+  if (out == nullptr || blobs == nullptr || noise_seed == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (n_blobs != 16 && n_blobs != 32 && n_blobs != 64) return ADCT_ERR_UNSUPPORTED;
+  cudaStream_t s = as_stream(stream);
+  const dim3 g((unsigned)((w + kThreads - 1) / kThreads), (unsigned)((h + kSynthRows - 1) / kSynthRows));
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    const dim3 gg(g.x, g.y, (unsigned)nf);
+    const u64* seeds = reinterpret_cast<const u64*>(noise_seed);
+    if (n_blobs == 16) k_synth<16><<<gg, kThreads, 0, s>>>(out, h, w, img_stride, blobs, seeds, f0);
+    else if (n_blobs == 32) k_synth<32><<<gg, kThreads, 0, s>>>(out, h, w, img_stride, blobs, seeds, f0);
+    else k_synth<64><<<gg, kThreads, 0, s>>>(out, h, w, img_stride, blobs, seeds, f0);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+// --- host pipeline -------------------------------------------------------------
+}  // extern "C"
+
+struct adct_pipeline {
+  int device = 0;
+  size_t chunk_bytes = 0;
+  static constexpr int kDepth = 3;
+  cudaStream_t stream[kDepth] = {};
+  uint8_t* d_in[kDepth] = {};
+  uint8_t* d_out[kDepth] = {};
+  uint64_t* d_sse[kDepth] = {};
+  int64_t sse_cap = 0;
+};
+
+namespace {
+
+void pipeline_free(adct_pipeline* p) {
+  for (int k = 0; k < adct_pipeline::kDepth; ++k) {
+    if (p->stream[k]) cudaStreamDestroy(p->stream[k]);
+    if (p->d_in[k]) cudaFree(p->d_in[k]);
+    if (p->d_out[k]) cudaFree(p->d_out[k]);
+    if (p->d_sse[k]) cudaFree(p->d_sse[k]);
+  }
+  delete p;
+}
+
+// kind: 0 retain (r), 1 quant (qtab)
+int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, int64_t n, int32_t h,
+                 int32_t w, int kind, int32_t r, const adct_qtab_t* qtab, uint64_t* host_sse) {
+  if (p == nullptr || n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (h < 0 || w < 0 || (h % 8) || (w % 8)) return ADCT_ERR_BAD_DIMENSIONS;
+  if (kind == 0 && (r < 1 || r > 64)) return ADCT_ERR_INVALID_RETENTION;
+  if (kind == 1 && qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (n == 0) return ADCT_OK;
+  if (host_img == nullptr || host_sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  const int64_t px = (int64_t)h * w;
+  if (px == 0) {
+    std::memset(host_sse, 0, (size_t)n * sizeof(uint64_t));
+    return ADCT_OK;
+  }
+  int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
+  if (per < 1) return ADCT_ERR_INVALID_ARGUMENT;  // chunk smaller than one image
+  if (per > p->sse_cap) per = p->sse_cap;
+  ADCT_CUDA_TRY(cudaSetDevice(p->device));
+  int64_t chunk = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += per, ++chunk) {
+    const int b = (int)(chunk % adct_pipeline::kDepth);
+    const int64_t m = (n - i0) < per ? (n - i0) : per;
+    cudaStream_t s = p->stream[b];
+    ADCT_CUDA_TRY(cudaMemcpyAsync(p->d_in[b], host_img + i0 * px, (size_t)(m * px),
+                                  cudaMemcpyHostToDevice, s));
+    uint8_t* drec = host_rec ? p->d_out[b] : nullptr;
+    int rc;
+    if (kind == 0)
+      rc = adct_compress_retain(p->d_in[b], drec, m, h, w, px, px, r, p->d_sse[b], nullptr, s);
+    else
+      rc = adct_compress_quant(p->d_in[b], drec, m, h, w, px, px, qtab, p->d_sse[b], s);
+    if (rc != ADCT_OK) return rc;
+    if (host_rec)
+      ADCT_CUDA_TRY(cudaMemcpyAsync(host_rec + i0 * px, p->d_out[b], (size_t)(m * px),
+                                    cudaMemcpyDeviceToHost, s));
+    ADCT_CUDA_TRY(cudaMemcpyAsync(host_sse + i0, p->d_sse[b], (size_t)m * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, s));
+  }
+  for (int k = 0; k < adct_pipeline::kDepth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+  return ADCT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int adct_pipeline_create(int32_t device, size_t chunk_bytes, adct_pipeline_t** out) {
+  if (out == nullptr || chunk_bytes < 64) return ADCT_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  adct_pipeline* p = new (std::nothrow) adct_pipeline();
+  if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  p->device = device;
+  p->chunk_bytes = (chunk_bytes + 15) / 16 * 16;
+  p->sse_cap = (int64_t)(p->chunk_bytes / 64);
+  cudaError_t e = cudaSetDevice(device);
+  for (int k = 0; e == cudaSuccess && k < adct_pipeline::kDepth; ++k) {
+    e = cudaStreamCreateWithFlags(&p->stream[k], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_in[k], p->chunk_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_out[k], p->chunk_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sse[k], (size_t)p->sse_cap * sizeof(uint64_t));
+  }
+  if (e != cudaSuccess) {
+    pipeline_free(p);
+    return cuda_fail(e);
+  }
+  *out = p;
+  return ADCT_OK;
+}
+
+int adct_pipeline_destroy(adct_pipeline_t* p) {
+  if (p == nullptr) return ADCT_OK;
+  pipeline_free(p);
+  return ADCT_OK;
+}
+
+int adct_pipeline_compress_retain(adct_pipeline_t* p, const uint8_t* host_img, uint8_t* host_rec,
+                                  int64_t n, int32_t h, int32_t w, int32_t r, uint64_t* host_sse) {
+  return pipeline_run(p, host_img, host_rec, n, h, w, 0, r, nullptr, host_sse);
+}
+
+int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img, uint8_t* host_rec,
+                                 int64_t n, int32_t h, int32_t w, const adct_qtab_t* qtab,
+                                 uint64_t* host_sse) {
+  return pipeline_run(p, host_img, host_rec, n, h, w, 1, 0, qtab, host_sse);
+}
+
+int adct_host_register(void* ptr, size_t bytes) {
+  if (ptr == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (bytes == 0) return ADCT_OK;
+  ADCT_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return ADCT_OK;
+}
+
+int adct_host_unregister(void* ptr) {
+  if (ptr == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  ADCT_CUDA_TRY(cudaHostUnregister(ptr));
+  return ADCT_OK;
+}
+
+}  // extern "C"

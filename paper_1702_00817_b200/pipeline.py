@@ -1,0 +1,100 @@
+"""Host-buffer pipeline: the end-to-end public call for images in CPU memory.
+
+Wraps the native adct_pipeline (csrc/capi.cu): chunks of the host batch are
+copied in, compressed and copied out on three CUDA streams so H2D, kernel
+and D2H overlap.  Host arrays are page-locked for the duration of the call
+(adct_host_register) unless already pinned.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import BadDimensions, InvalidRetention
+
+
+class HostPipeline:
+    def __init__(self, device: int = 0, chunk_bytes: int = 256 << 20):
+        h = ctypes.c_void_p()
+        _lib.call("adct_pipeline_create", int(device), int(chunk_bytes), ctypes.byref(h))
+        self._h = h
+
+    def close(self) -> None:
+        if self._h:
+            _lib.call("adct_pipeline_destroy", self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _check(images: np.ndarray) -> tuple[int, int, int]:
+        if images.dtype != np.uint8 or images.ndim != 3 or not images.flags.c_contiguous:
+            raise ValueError("images must be a C-contiguous uint8 array (N, H, W)")
+        n, h, w = images.shape
+        if h % 8 or w % 8:
+            raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+        return n, h, w
+
+    def compress_retain(self, images: np.ndarray, r: int, rec: np.ndarray | None = None, *, register: bool = True):
+        """Returns (rec or None, sse int64[N])."""
+        if not 1 <= int(r) <= 64:
+            raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+        n, h, w = self._check(images)
+        sse = np.zeros(n, dtype=np.uint64)
+        with _Pinned([images, rec] if register else []):
+            _lib.call(
+                "adct_pipeline_compress_retain", self._h, images.ctypes.data,
+                None if rec is None else rec.ctypes.data, n, h, w, int(r), sse.ctypes.data,
+            )
+        return rec, sse.astype(np.int64)
+
+    def compress_quant(self, images: np.ndarray, qtab, rec: np.ndarray | None = None, *, register: bool = True):
+        n, h, w = self._check(images)
+        sse = np.zeros(n, dtype=np.uint64)
+        with _Pinned([images, rec] if register else []):
+            _lib.call(
+                "adct_pipeline_compress_quant", self._h, images.ctypes.data,
+                None if rec is None else rec.ctypes.data, n, h, w, ctypes.byref(qtab), sse.ctypes.data,
+            )
+        return rec, sse.astype(np.int64)
+
+
+class _Pinned:
+    """Page-lock numpy buffers for the duration of a call."""
+
+    def __init__(self, arrays):
+        self.arrays = [a for a in arrays if a is not None and a.nbytes > 0]
+        self.done = []
+
+    def __enter__(self):
+        for a in self.arrays:
+            _lib.call("adct_host_register", a.ctypes.data, a.nbytes)
+            self.done.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        for a in self.done:
+            _lib.lib().adct_host_unregister(a.ctypes.data)
+        self.done = []
+
+
+def pin(array: np.ndarray) -> None:
+    """Page-lock an array for repeated pipeline calls (unpin() to release)."""
+    _lib.call("adct_host_register", array.ctypes.data, array.nbytes)
+
+
+def unpin(array: np.ndarray) -> None:
+    _lib.call("adct_host_unregister", array.ctypes.data)

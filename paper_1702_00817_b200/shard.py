@@ -1,0 +1,91 @@
+"""Batch sharding across the GPUs of one box (north-star subsystem 5).
+
+Images (or video frames) are independent, so rank k of N owns the contiguous
+range [k*n/N, (k+1)*n/N) and runs the fused kernel on it with no data-path
+communication.  The only exchange is one all-reduce(SUM) of the per-image
+int64 SSE vector (each rank fills its slice, zeros elsewhere), after which
+every rank holds the exact global SSE and PSNR — bit-identical for any N
+because integer sums are order independent.
+
+torch.distributed is the plumbing: NCCL over NVLink/NVSwitch on the B200 box,
+gloo on CPU for the multi-rank tests.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    start: int
+    stop: int
+
+    @property
+    def count(self) -> int:
+        return self.stop - self.start
+
+
+def shard_range(n: int, rank: int, world: int) -> Shard:
+    """Contiguous balanced split: sizes differ by at most one, earlier ranks larger."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise ValueError(f"bad shard request n={n} rank={rank} world={world}")
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    stop = start + base + (1 if rank < extra else 0)
+    return Shard(rank, world, start, stop)
+
+
+def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
+    """(rank, world, local_rank) from torchrun's environment; initialises the
+    default process group when WORLD_SIZE > 1 (NCCL if CUDA, else gloo)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
+def global_sse(local_sse: torch.Tensor, shard: Shard, n_total: int, group=None) -> torch.Tensor:
+    """Scatter this rank's per-unit SSE into a zero int64[n_total, ...] vector and
+    all-reduce(SUM) it; returns the global vector (identical on every rank)."""
+    full = torch.zeros((n_total,) + tuple(local_sse.shape[1:]), dtype=torch.int64, device=local_sse.device)
+    full[shard.start : shard.stop] = local_sse
+    if shard.world > 1:
+        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    return full
+
+
+def run_sharded(
+    n_total: int,
+    compute: Callable[[Shard], torch.Tensor],
+    *,
+    rank: int | None = None,
+    world: int | None = None,
+    group=None,
+) -> torch.Tensor:
+    """Run `compute(shard)` (-> int64 SSE for the shard's units) on this rank's
+    range and return the all-reduced global SSE."""
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    sh = shard_range(n_total, rank, world)
+    local = compute(sh)
+    if local.shape[0] != sh.count:
+        raise ValueError(f"compute returned {local.shape[0]} rows for a shard of {sh.count}")
+    return global_sse(local, sh, n_total, group)

@@ -1,0 +1,120 @@
+"""GPU parity: CUDA path (through the C ABI) vs the CPU oracle, bit-exact."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import exact
+from paper_1702_00817_b200 import batch, quant, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _imgs(cuda, seeds, h=512, w=512, cfg=0):
+    nb, smin, smax = synth.CONFIG_BLOBS[cfg]
+    return synth.images_device(seeds, h, w, nb, smin, smax, device=cuda)
+
+
+def test_forward_int32_config0(cuda):
+    x = _imgs(cuda, [0])
+    z = batch.forward_int(x)
+    torch.cuda.synchronize()
+    want = exact.forward_unscaled(x.cpu().numpy())
+    assert z.shape == (1, 4096, 8, 8)
+    assert np.array_equal(z.cpu().numpy().astype(np.int64), want)
+
+
+@pytest.mark.parametrize("level_shift", [False, True])
+@pytest.mark.parametrize("shape", [(2, 64, 64), (3, 40, 24), (1, 8, 8), (2, 16, 48)])
+def test_forward_int_shapes(cuda, shape, level_shift):
+    g = torch.Generator(device="cpu").manual_seed(sum(shape))
+    x = torch.randint(0, 256, shape, dtype=torch.uint8, generator=g).to(cuda)
+    for dt in (torch.int32, torch.int16):
+        z = batch.forward_int(x, level_shift=level_shift, dtype=dt)
+        torch.cuda.synchronize()
+        want = exact.forward_unscaled(x.cpu().numpy(), level_shift=level_shift)
+        assert np.array_equal(z.cpu().numpy().astype(np.int64), want)
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 6, 10, 15, 25, 36, 45, 55, 63, 64])
+def test_retain_matches_oracle(cuda, r):
+    x = _imgs(cuda, [3, 4])
+    rec, sse, ssef = batch.compress_retain(x, r, unrounded_sse=True)
+    rec2, sse2, _ = batch.compress_retain(x, r)
+    torch.cuda.synchronize()
+    want_rec, want_sse, want_ssef = exact.compress_retain(x.cpu().numpy(), r)
+    assert np.array_equal(rec.cpu().numpy(), want_rec)
+    assert np.array_equal(rec2.cpu().numpy(), want_rec)  # pruned kernel == runtime-r kernel
+    assert np.array_equal(sse.cpu().numpy(), want_sse)
+    assert np.array_equal(sse2.cpu().numpy(), want_sse)
+    assert np.array_equal(ssef.cpu().numpy(), want_ssef)
+
+
+@pytest.mark.parametrize("r", list(range(1, 65)))
+def test_retain_every_r_random_noise(cuda, r):
+    """Full-range random pixels stress the 16-bit-lane bounds for every r."""
+    g = torch.Generator().manual_seed(r)
+    x = torch.randint(0, 256, (2, 64, 128), dtype=torch.uint8, generator=g)
+    x[0, :32] = 255 * (x[0, :32] > 127)  # saturated edges
+    xd = x.to(cuda)
+    rec, sse, _ = batch.compress_retain(xd, r)
+    torch.cuda.synchronize()
+    want_rec, want_sse, _ = exact.compress_retain(x.numpy(), r)
+    assert np.array_equal(rec.cpu().numpy(), want_rec)
+    assert np.array_equal(sse.cpu().numpy(), want_sse)
+
+
+@pytest.mark.parametrize("q", [1, 5, 10, 25, 50, 75, 90, 100])
+def test_quant_matches_oracle(cuda, q):
+    x = _imgs(cuda, [7, 8], 256, 256, cfg=2)
+    g = torch.Generator().manual_seed(q)
+    noise = torch.randint(0, 256, (1, 256, 256), dtype=torch.uint8, generator=g).to(cuda)
+    x = torch.cat([x, noise])
+    qt = quant.quant_table(q)
+    rec, sse = batch.compress_quant(x, qt)
+    torch.cuda.synchronize()
+    want_rec, want_sse = exact.compress_quant(x.cpu().numpy(), exact.qprime(quant.q50_luma(), q))
+    assert np.array_equal(rec.cpu().numpy(), want_rec)
+    assert np.array_equal(sse.cpu().numpy(), want_sse)
+
+
+def test_ragged_width_retain_and_quant(cuda):
+    g = torch.Generator().manual_seed(11)
+    x = torch.randint(0, 256, (3, 24, 40), dtype=torch.uint8, generator=g)  # W % 16 == 8
+    xd = x.to(cuda)
+    rec, sse, _ = batch.compress_retain(xd, 10)
+    qt = quant.quant_table(50)
+    recq, sseq = batch.compress_quant(xd, qt)
+    torch.cuda.synchronize()
+    wr, ws, _ = exact.compress_retain(x.numpy(), 10)
+    wq, wqs = exact.compress_quant(x.numpy(), exact.qprime(quant.q50_luma(), 50))
+    assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws)
+    assert np.array_equal(recq.cpu().numpy(), wq) and np.array_equal(sseq.cpu().numpy(), wqs)
+
+
+def test_planes_quant_one_launch(cuda):
+    g = torch.Generator().manual_seed(5)
+    y = torch.randint(0, 256, (2, 64, 96), dtype=torch.uint8, generator=g)
+    cb = torch.randint(0, 256, (2, 32, 48), dtype=torch.uint8, generator=g)
+    cr = torch.randint(0, 256, (2, 32, 48), dtype=torch.uint8, generator=g)
+    qt = quant.quant_table(75)
+    recs, sse = batch.compress_quant_planes([y.to(cuda), cb.to(cuda), cr.to(cuda)], qt)
+    torch.cuda.synchronize()
+    qp = exact.qprime(quant.q50_luma(), 75)
+    for k, p in enumerate((y, cb, cr)):
+        wr, ws = exact.compress_quant(p.numpy(), qp)
+        assert np.array_equal(recs[k].cpu().numpy(), wr)
+        assert np.array_equal(sse[:, k].cpu().numpy(), ws)
+
+
+def test_sweep_matches_oracle(cuda):
+    x = _imgs(cuda, [0, 1, 2], 128, 128)
+    s = batch.sweep_retain_sse(x, 1, 45)
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy(), exact.sweep_sse(x.cpu().numpy(), 1, 45))
+
+
+def test_empty_batch(cuda):
+    x = torch.empty((0, 64, 64), dtype=torch.uint8, device=cuda)
+    rec, sse, _ = batch.compress_retain(x, 10)
+    assert rec.shape == (0, 64, 64) and sse.shape == (0,)
