@@ -61,20 +61,31 @@ int adct_last_cuda_error(void);
  * BASELINE.json specifies.  The device quantiser computes
  *   q = sign(Z) * floor((2|Z| + Q') / (2 Q'))      (round half away from zero)
  *   Z' = q * Q'
- * exactly with one multiply-high per coefficient; `magic`, `kbias` and
- * `uoff` are the constants that make it exact, verified exhaustively over
- * every reachable |Z| by adct_qtab_build.  Treat the struct as opaque except
- * for `qprime`, `wide` and `max_abs_v`.
+ * exactly with one multiply-high per coefficient; the constants below make
+ * it exact and are verified exhaustively over every reachable coefficient
+ * (|Z| <= 8192) by adct_qtab_build.  Treat the struct as opaque except for
+ * `qprime`, `qe`, `wide`, `max_abs_v` and `aligned`.
  * ------------------------------------------------------------------------- */
 typedef struct adct_qtab {
   int32_t qprime[64];   /* rounded Q', row-major (u*8+v) */
-  uint32_t magic[64];   /* floor(U / (2Q')) == umulhi(U, magic) on the reachable U range */
-  int32_t kbias[64];    /* K: U = 2Z - [Z<0] + Q'(2K+1) >= 0, quotient offset */
   int32_t qe[64];       /* Q' * E[u][v], E = 64 d[u]^2 d[v]^2 in {1,2,4,8,16} */
-  int32_t wide;         /* 1: 16-bit-lane inverse not provably exact -> 32-bit inverse kernel */
-  int32_t max_abs_v;    /* proven bound of |64*(x_rec-128)| before clamping */
+  /* Two-lane quantiser (wide == 0): for each 16-bit lane Z,
+   *   U = (Z + bias) * mult + [Z >= 0],  q = umulhi(U, magic) - kq,
+   * mult = 2 and divisor 2Q' for odd Q', mult = 1 and divisor Q' for even Q'. */
+  uint32_t magic[64];
+  int32_t bias[64];
+  int32_t mult[64];
+  int32_t kq[64];
+  /* Scalar quantiser (any table): U = 2Z - [Z<0] + cadd,
+   *   q = (umulhi(U, magic_w) >> shift_w) - kw. */
+  uint32_t magic_w[64];
+  int32_t cadd_w[64];
+  int32_t kw[64];
+  int32_t shift_w[64];
+  int32_t wide;         /* 1: 16-bit-lane inverse not provably exact -> one block per thread */
+  int32_t max_abs_v;    /* proven bound of |64*(x_hat-128)| before clamping */
   int32_t quality;      /* JPEG quality used to build it, or -1 for an explicit table */
-  int32_t reserved;
+  int32_t aligned;      /* 1: max_abs_v + 32 <= 24576, output window needs no bit flip */
 } adct_qtab_t;
 
 /* Build from an unrounded Q' table (64 float64, row-major), i.e. the output of

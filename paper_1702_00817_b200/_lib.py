@@ -26,13 +26,19 @@ class QTab(ctypes.Structure):
 
     _fields_ = [
         ("qprime", c_int32 * 64),
-        ("magic", ctypes.c_uint32 * 64),
-        ("kbias", c_int32 * 64),
         ("qe", c_int32 * 64),
+        ("magic", ctypes.c_uint32 * 64),
+        ("bias", c_int32 * 64),
+        ("mult", c_int32 * 64),
+        ("kq", c_int32 * 64),
+        ("magic_w", ctypes.c_uint32 * 64),
+        ("cadd_w", c_int32 * 64),
+        ("kw", c_int32 * 64),
+        ("shift_w", c_int32 * 64),
         ("wide", c_int32),
         ("max_abs_v", c_int32),
         ("quality", c_int32),
-        ("reserved", c_int32),
+        ("aligned", c_int32),
     ]
 
 

@@ -242,27 +242,37 @@ __device__ __forceinline__ void unpack_unit(const uint4 (&w)[8], u32 (&x)[8][8])
   }
 }
 
-// Output fields U = 64(x_hat-128) + 32 + 32768 (two unsigned 16-bit lanes)
-// -> reconstructed bytes.  pixel = clamp(floor((U - 24576) / 64), 0, 255):
-// clamp U to [0x6000, 0x9FFF] (native VIMNMX.U16x2), shift so bits 6..13 of
-// each lane land in bytes 1 and 3, gather with PRMT, and flip bit 7
-// ((U>>6) & 0xFF == pixel ^ 0x80 on the clamped range).
+// Output fields -> reconstructed bytes.  Each 16-bit field holds
+// U = 64(x_hat-128) + 32 + O (unsigned, no borrow between lanes), and
+// pixel = clamp(floor((U - O + 8192) / 64), 0, 255).
+//   FLIP (O = 32768): clamp U to [0x6000, 0x9FFF] (native VIMNMX.U16x2);
+//     (U >> 6) & 0xFF == pixel ^ 0x80, so the packed word is XORed with 0x80.
+//   !FLIP (O = 24576, tables whose proven range allows it): clamp to
+//     [0x4000, 0x7FFF]; (U >> 6) & 0xFF == pixel, no fix-up.
+// Shifting by 2 puts bits 6..13 of each lane in bytes 1 and 3 (the bits
+// pushed from lane A into lane B land in byte 2, which is never read), then
+// PRMT gathers the bytes.
+template <bool FLIP>
 __device__ __forceinline__ u32 clamp_shift(u32 U) {
-  return __vmaxu2(__vminu2(U, 0x9FFF9FFFu), 0x60006000u) << 2;
+  constexpr u32 lo = FLIP ? 0x60006000u : 0x40004000u;
+  constexpr u32 hi = FLIP ? 0x9FFF9FFFu : 0x7FFF7FFFu;
+  return __vmaxu2(__vminu2(U, hi), lo) << 2;
 }
 
+template <bool FLIP = true>
 __device__ __forceinline__ void pack_row(const u32 (&U)[8], uint4& out) {
-  const u32 s0 = clamp_shift(U[0]), s1 = clamp_shift(U[1]), s2 = clamp_shift(U[2]),
-            s3 = clamp_shift(U[3]), s4 = clamp_shift(U[4]), s5 = clamp_shift(U[5]),
-            s6 = clamp_shift(U[6]), s7 = clamp_shift(U[7]);
+  const u32 s0 = clamp_shift<FLIP>(U[0]), s1 = clamp_shift<FLIP>(U[1]), s2 = clamp_shift<FLIP>(U[2]),
+            s3 = clamp_shift<FLIP>(U[3]), s4 = clamp_shift<FLIP>(U[4]), s5 = clamp_shift<FLIP>(U[5]),
+            s6 = clamp_shift<FLIP>(U[6]), s7 = clamp_shift<FLIP>(U[7]);
   const u32 q0 = __byte_perm(s0, s1, 0x7531);  // a0 b0 a1 b1
   const u32 q1 = __byte_perm(s2, s3, 0x7531);  // a2 b2 a3 b3
   const u32 q2 = __byte_perm(s4, s5, 0x7531);
   const u32 q3 = __byte_perm(s6, s7, 0x7531);
-  out.x = __byte_perm(q0, q1, 0x6420) ^ 0x80808080u;  // a0 a1 a2 a3
-  out.y = __byte_perm(q2, q3, 0x6420) ^ 0x80808080u;  // a4 .. a7
-  out.z = __byte_perm(q0, q1, 0x7531) ^ 0x80808080u;  // b0 .. b3
-  out.w = __byte_perm(q2, q3, 0x7531) ^ 0x80808080u;  // b4 .. b7
+  constexpr u32 fx = FLIP ? 0x80808080u : 0u;
+  out.x = __byte_perm(q0, q1, 0x6420) ^ fx;  // a0 a1 a2 a3
+  out.y = __byte_perm(q2, q3, 0x6420) ^ fx;  // a4 .. a7
+  out.z = __byte_perm(q0, q1, 0x7531) ^ fx;  // b0 .. b3
+  out.w = __byte_perm(q2, q3, 0x7531) ^ fx;  // b4 .. b7
 }
 
 // Sum of squared byte differences of 4 pixel pairs: |a-b| per byte (VABSDIFF4),
@@ -273,14 +283,14 @@ __device__ __forceinline__ u32 sse4(u32 a, u32 b, u32 acc) {
 }
 
 // Store reconstructed rows and accumulate SSE (per-thread partial).
-template <bool PAIR>
+template <bool PAIR, bool FLIP = true>
 __device__ __forceinline__ u32 emit_unit(const u32 (&U)[8][8], const uint4 (&w)[8],
                                          uint8_t* dst, int32_t width) {
   u32 acc = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     uint4 o;
-    pack_row(U[i], o);
+    pack_row<FLIP>(U[i], o);
     if (dst != nullptr) {
       if (PAIR)
         st_stream16(dst + (int64_t)i * width, o);
@@ -297,21 +307,13 @@ __device__ __forceinline__ u32 emit_unit(const u32 (&U)[8][8], const uint4 (&w)[
   return acc;
 }
 
-// Block-wide sum of a per-thread u32 partial, one 64-bit atomic per CTA.
+// Sum of a per-thread u32 partial over the warp (REDUX), one 64-bit atomic
+// per warp.  No CTA barrier: warps that finish early leave immediately.
 // Per-thread partials are <= 128 * 255^2 < 2^24, per-warp sums < 2^29.
+// All threads of a CTA target the same image/plane (tiles never straddle).
 __device__ __forceinline__ void block_add_u32(u32 v, u64* dst) {
-  __shared__ u32 warp_sums[kThreads / 32];
   v = __reduce_add_sync(0xffffffffu, v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) warp_sums[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    u64 t = 0;
-#pragma unroll
-    for (int k = 0; k < kThreads / 32; ++k) t += warp_sums[k];
-    if (t != 0) atomicAdd(dst, t);
-  }
-  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && v != 0) atomicAdd(dst, (u64)v);
 }
 
 __device__ __forceinline__ void block_add_u64(u64 v, u64* dst) {

@@ -11,33 +11,34 @@ namespace adct {
 // Filled from adct_qtab_t by the host (capi.cu).
 // ---------------------------------------------------------------------------
 struct QParamsDev {
-  u32 magic[64];  // umulhi(U, magic) == floor(U / 2Q'), verified exhaustively
-  u32 cadd[64];   // C = Q'(2K+1)
+  u32 magic[64];  // umulhi(U, magic) == floor(U / divisor), verified exhaustively
+  u32 bpk[64];    // per-position bias B, both lanes (B * 65537)
+  u32 mult[64];   // 2 (odd Q', divisor 2Q') or 1 (even Q', divisor Q')
   u32 qe[64];     // Q' * E[u][v]
-  u32 wadd[64];   // -K*qe*65537 (+0x80208020 at DC: rounding +32, lane bias)
-  int32_t kbias[64];
+  u32 wadd[64];   // -kq*qe*65537 (+ (O+32)*65537 at DC: rounding, output offset)
 };
 
-// Per-position pre-quantisation bias on the linear form: lane bias 0x8000 on
-// lane A (so lane A's 16-bit field is unsigned and lane B has no borrow), plus
-// the level shift -8192 on the DC coefficient of both lanes
-// (T (X-128) T^T = Z - 8192 e0 e0^T).
-__device__ __forceinline__ constexpr u32 qbias(int p) {
-  return p == 0 ? (0x8000u - 8192u * 65537u) : 0x8000u;
-}
+struct QParamsWide {  // scalar quantiser of k_quant_wide
+  u32 magic[64];
+  u32 cadd[64];
+  int32_t kbias[64];
+  int32_t shift[64];
+  int32_t qe[64];
+};
 
-// Round-half-away quotient + K of both lanes.  For true Z:
-//   U = 2Z - [Z<0] + C   (>= 0),   q + K = floor(U / 2Q') = umulhi(U, magic).
-// Lane A is held as lo = Z_A + 32768 in [0, 65535]:
-//   U_A = 2 lo + (lo >> 15) + (C - 65537).
-__device__ __forceinline__ void quant_lanes(u32 z, int p, const QParamsDev& q, u32& qa, u32& qb) {
-  const u32 v = z + qbias(p);
-  const u32 lo = v & 0xFFFFu;
-  const int hi = (int)v >> 16;
-  const u32 ua = 2u * lo + (lo >> 15) + (q.cadd[p] - 65537u);
-  const u32 ub = (u32)(2 * hi + (hi >> 31)) + q.cadd[p];
-  qa = __umulhi(ua, q.magic[p]);
-  qb = __umulhi(ub, q.magic[p]);
+// Quantise + dequantise one coefficient position of both blocks, returning
+// W = E o (q Q') in linear form.  z = T(X-128)T^T in linear form (lanes
+// |Z| <= 8192).  Lane signs are bits 15 and 31 of z: bit 15 is exactly the
+// sign of lane A; bit 31 is the sign of lane B minus A's borrow, which only
+// errs when Z_B == 0, where both tie-breaks give q = 0 (host-verified).
+//   U = (Z + B) * mult + [Z >= 0]   (both 16-bit fields, no carry)
+//   q + kq = umulhi(U, magic)       (exact, adct_qtab_build)
+__device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
+  const u32 s = ((z >> 15) & 0x10001u) ^ 0x10001u;
+  const u32 U = (z + q.bpk[p]) * q.mult[p] + s;
+  const u32 qa = __umulhi(U & 0xFFFFu, q.magic[p]);
+  const u32 qb = __umulhi(U >> 16, q.magic[p]);
+  return (qa + (qb << 16)) * q.qe[p] + q.wadd[p];
 }
 
 // ---------------------------------------------------------------------------
@@ -106,59 +107,50 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
-// K3: fused quantised pipeline.  WIDE=false: 16-bit lanes end to end (exact
-// when the host proved |64(x_hat-128)+32| <= 32767 for the table);
-// WIDE=true: 32-bit inverse per block for coarse tables (e.g. q=10).
+// K3: fused quantised pipeline, 16-bit lanes end to end (exact when the host
+// proved |64(x_hat-128)+32| <= 32767 for the table, adct_qtab_t.wide == 0).
 // ---------------------------------------------------------------------------
-template <bool PAIR, bool WIDE>
-__global__ void __launch_bounds__(kThreads)
+template <bool PAIR, bool FLIP>
+__global__ void __launch_bounds__(kThreads, 2)
     k_quant(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
+  // Original pixel words wait in shared memory for the SSE (frees 32
+  // registers); each thread only reads back its own slots, so no barrier.
+  __shared__ uint4 s_orig[8][kThreads];
   UnitLoc L;
   u32 acc = 0;
   if (locate_unit<PAIR>(ps, L)) {
     uint4 w[8];
     load_unit<PAIR>(L.src, L.width, w);
-    u32 x[8][8], Z[8][8], U[8][8];
+    u32 x[8][8], U[8][8];
     unpack_unit(w, x);
-    fwd2d(x, Z);
-    if (!WIDE) {
-      u32 W[8][8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+    for (int i = 0; i < 8; ++i) s_orig[i][threadIdx.x] = w[i];
+    {
+      // Streamed 2-D transform: row pass, then per column v: forward column,
+      // quantise/dequantise its 8 coefficients, inverse column; then rows.
+      u32 t[8][8], c[8][8];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int p = u * 8 + v;
-          u32 qa, qb;
-          quant_lanes(Z[u][v], p, q, qa, qb);
-          W[u][v] = (qa + (qb << 16)) * q.qe[p] + q.wadd[p];
-        }
-      inv2d(W, U);
-    } else {
-      int Wa[8][8], Wb[8][8], Va[8][8], Vb[8][8];
+      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int v = 0; v < 8; ++v) {
+        u32 col[8], Zc[8], Wc[8], cc[8];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const int p = u * 8 + v;
-          u32 qa, qb;
-          quant_lanes(Z[u][v], p, q, qa, qb);
-          Wa[u][v] = ((int)qa - q.kbias[p]) * (int)q.qe[p];
-          Wb[u][v] = ((int)qb - q.kbias[p]) * (int)q.qe[p];
-        }
-      Wa[0][0] += 32;
-      Wb[0][0] += 32;
-      inv2d(Wa, Va);
-      inv2d(Wb, Vb);
+        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+        fwd8(col, Zc);
+        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift: T(X-128)T^T = Z - 8192 e0 e0^T
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+        for (int u = 0; u < 8; ++u) Wc[u] = quant_pair(Zc[u], u * 8 + v, q);
+        inv8(Wc, cc);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int a = min(max(Va[i][j], -8192), 8191) + 32768;
-          const int b = min(max(Vb[i][j], -8192), 8191) + 32768;
-          U[i][j] = (u32)a | ((u32)b << 16);
-        }
+        for (int i = 0; i < 8; ++i) c[i][v] = cc[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) inv8(c[i], U[i]);
     }
-    acc = emit_unit<PAIR>(U, w, L.dst, L.width);
+    uint4 wo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wo[i] = s_orig[i][threadIdx.x];
+    acc = emit_unit<PAIR, FLIP>(U, wo, L.dst, L.width);
   }
   if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
@@ -287,6 +279,59 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 #ifdef ADCT_DEFINE_PLAIN_KERNELS  // non-template kernels: defined once, in capi.cu
+// K3 for coarse tables (wide == 1, e.g. q < 25): one block per thread.  The
+// B lane is empty, so the "linear form" is a plain int32 and every
+// intermediate is exact whatever its magnitude.
+__global__ void __launch_bounds__(kThreads)
+    k_quant_wide(PlaneSetDev ps, const __grid_constant__ QParamsWide q, u64* __restrict__ sse) {
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<false>(ps, L)) {
+    uint4 w[8];
+    load_unit<false>(L.src, L.width, w);
+    int x[8][8], t[8][8], c[8][8], V[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        x[i][j] = (int)__byte_perm(j < 4 ? w[i].x : w[i].y, 0u, 0x4440 | (j & 3));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      int col[8], Zc[8], Wc[8], cc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+      fwd8(col, Zc);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int p = u * 8 + v;
+        const int z = Zc[u] - (p == 0 ? 8192 : 0);  // level shift
+        const u32 U = (u32)(2 * z + (z >> 31)) + q.cadd[p];
+        const int qq = (int)(__umulhi(U, q.magic[p]) >> q.shift[p]) - q.kbias[p];
+        Wc[u] = qq * q.qe[p] + (p == 0 ? 32 + 8192 : 0);  // rounding, +128 back
+      }
+      inv8(Wc, cc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i][v] = cc[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) inv8(c[i], V[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      u32 px[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) px[j] = (u32)min(max(V[i][j] >> 6, 0), 255);
+      const u32 lo = __byte_perm(__byte_perm(px[0], px[1], 0x0040), __byte_perm(px[2], px[3], 0x0040), 0x5410);
+      const u32 hi = __byte_perm(__byte_perm(px[4], px[5], 0x0040), __byte_perm(px[6], px[7], 0x0040), 0x5410);
+      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width, make_uint2(lo, hi));
+      acc = sse4(w[i].x, lo, acc);
+      acc = sse4(w[i].y, hi, acc);
+    }
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+}
+
 // ---------------------------------------------------------------------------
 // Float64 transforms (real-valued inputs; signature parity with the
 // reference's float API).  One thread per 8x8 block.

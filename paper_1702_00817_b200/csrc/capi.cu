@@ -39,13 +39,14 @@ struct PlaneSetHost {
   bool pair = true;
 };
 
-// Validate planes and lay out the tile grid.  `force_single` disables the
-// two-blocks-per-thread path (used by kernels without a PAIR=false variant).
-int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, PlaneSetHost& out) {
+// Validate planes and lay out the tile grid.  `force_single` selects one
+// block per thread (used by k_quant_wide).
+int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, PlaneSetHost& out,
+                 bool force_single = false) {
   if (planes == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
     return ADCT_ERR_INVALID_ARGUMENT;
   std::memset(&out.dev, 0, sizeof(out.dev));
-  bool pair = true;
+  bool pair = !force_single;
   for (int k = 0; k < n_planes; ++k) {
     const adct_plane_t& p = planes[k];
     if (p.height < 0 || p.width < 0 || (p.height % 8) != 0 || (p.width % 8) != 0)
@@ -113,14 +114,27 @@ int for_frame_chunks(PlaneSetHost& ps, int64_t n_frames, F&& launch) {
 
 QParamsDev to_qparams(const adct_qtab_t& t) {
   QParamsDev q;
+  const uint32_t dc_out = t.aligned ? 24576u : 32768u;  // output-field offset (see pack_row)
   for (int p = 0; p < 64; ++p) {
     q.magic[p] = t.magic[p];
-    q.cadd[p] = (uint32_t)t.qprime[p] * (2u * (uint32_t)t.kbias[p] + 1u);
+    q.bpk[p] = (uint32_t)t.bias[p] * 65537u;
+    q.mult[p] = (uint32_t)t.mult[p];
     q.qe[p] = (uint32_t)t.qe[p];
-    q.wadd[p] = (uint32_t)0 - (uint32_t)t.kbias[p] * (uint32_t)t.qe[p] * 65537u;
-    q.kbias[p] = t.kbias[p];
+    q.wadd[p] = (uint32_t)0 - (uint32_t)t.kq[p] * (uint32_t)t.qe[p] * 65537u;
   }
-  q.wadd[0] += (32768u + 32u) * 65537u;
+  q.wadd[0] += (dc_out + 32u) * 65537u;
+  return q;
+}
+
+QParamsWide to_qparams_wide(const adct_qtab_t& t) {
+  QParamsWide q;
+  for (int p = 0; p < 64; ++p) {
+    q.magic[p] = t.magic_w[p];
+    q.cadd[p] = (uint32_t)t.cadd_w[p];
+    q.kbias[p] = t.kw[p];
+    q.shift[p] = t.shift_w[p];
+    q.qe[p] = t.qe[p];
+  }
   return q;
 }
 
@@ -136,36 +150,87 @@ inline double ref_d(int u) {
   return (u & 1) ? s2 : ((u & 2) ? 0.5 : s8);
 }
 
+// round half away from zero of z / q, exact integer arithmetic
+inline int64_t rha_div(int64_t z, int64_t q) {
+  const int64_t a = (2 * (z < 0 ? -z : z) + q) / (2 * q);
+  return z < 0 ? -a : a;
+}
+
 int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out) {
   std::memset(out, 0, sizeof(*out));
   constexpr int64_t kZmax = 8192;  // |T (X-128) T^T| <= 128 n_u n_v <= 8192
+  bool packed_ok = true;
   for (int p = 0; p < 64; ++p) {
     const int u = p >> 3, v = p & 7;
     const int64_t Q = qp[p];
     if (Q < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
     if (Q > (1 << 20)) return ADCT_ERR_UNSUPPORTED;
     const int64_t E = 64 / (row_nnz(u) * row_nnz(v));
-    const int64_t D = 2 * Q;
-    int64_t K = (2 * kZmax + 1 - Q + D - 1) / D;  // ceil((2 Zmax + 1 - Q) / 2Q)
-    if (K < 0) K = 0;
-    const int64_t C = Q * (2 * K + 1);
-    const uint64_t magic = ((1ull << 32) + (uint64_t)D - 1) / (uint64_t)D;  // ceil(2^32 / D)
-    if (magic > 0xFFFFFFFFull) return ADCT_ERR_UNSUPPORTED;
-    if (C + 2 * kZmax >= (1ll << 32)) return ADCT_ERR_UNSUPPORTED;
-    // Exhaustive verification over every reachable coefficient value.
-    for (int64_t Z = -kZmax; Z <= kZmax; ++Z) {
-      const int64_t U = 2 * Z - (Z < 0 ? 1 : 0) + C;
-      if (U < 0) return ADCT_ERR_UNSUPPORTED;
-      const uint64_t got = ((uint64_t)U * magic) >> 32;
-      const int64_t q = (2 * (Z < 0 ? -Z : Z) + Q) / D;  // round half away of |Z|/Q
-      const int64_t want = (Z < 0 ? -q : q) + K;
-      if ((int64_t)got != want) return ADCT_ERR_UNSUPPORTED;
-    }
-    out->qprime[p] = (int32_t)Q;
-    out->magic[p] = (uint32_t)magic;
-    out->kbias[p] = (int32_t)K;
     if (Q * E > 0x7FFFFFFF / 4) return ADCT_ERR_UNSUPPORTED;
+    out->qprime[p] = (int32_t)Q;
     out->qe[p] = (int32_t)(Q * E);
+
+    // Two-lane quantiser: U = (Z + B) * mult + [Z >= 0] must fit 16 bits.
+    // Odd Q': U = 2Z + Q' - [Z<0] + 2Q' K, divisor 2Q'.  Even Q': ties of
+    // (2Z + Q' - [Z<0]) / 2Q' cannot hit the odd numerator, so
+    // floor((Z + Q'/2 - [Z<0]) / Q') is the same quotient, divisor Q'.
+    if (Q <= 8191) {
+      const bool odd = (Q & 1) != 0;
+      const int64_t mult = odd ? 2 : 1, D = odd ? 2 * Q : Q;
+      const int64_t b0 = odd ? (Q - 1) / 2 : Q / 2 - 1;
+      int64_t K1 = (kZmax - b0 + Q - 1) / Q;
+      if (K1 < 0) K1 = 0;
+      const int64_t B = b0 + Q * K1;
+      const uint64_t m = ((1ull << 32) + (uint64_t)D - 1) / (uint64_t)D;
+      bool ok = m <= 0xFFFFFFFFull;
+      for (int64_t Z = -kZmax; ok && Z <= kZmax; ++Z) {
+        // s = [Z >= 0]; at Z == 0 the kernel's lane-B sign bit may read 1
+        // (borrow from a negative lane A), so both values must agree there.
+        for (int s = (Z == 0 ? 0 : (Z > 0 ? 1 : 0)); s <= (Z >= 0 ? 1 : 0); ++s) {
+          const int64_t U = (Z + B) * mult + s;
+          if (U < 0 || U > 0xFFFF) { ok = false; break; }
+          const int64_t got = (int64_t)(((uint64_t)U * m) >> 32) - K1;
+          if (got != rha_div(Z, Q)) { ok = false; break; }
+        }
+      }
+      if (ok) {
+        out->magic[p] = (uint32_t)m;
+        out->bias[p] = (int32_t)B;
+        out->mult[p] = (int32_t)mult;
+        out->kq[p] = (int32_t)K1;
+      } else {
+        packed_ok = false;
+      }
+    } else {
+      packed_ok = false;
+    }
+
+    // Scalar quantiser: U = 2Z - [Z<0] + C, C = Q'(2K+1), divisor 2Q'.
+    {
+      const int64_t D = 2 * Q;
+      int64_t K = (2 * kZmax + 1 - Q + D - 1) / D;
+      if (K < 0) K = 0;
+      const int64_t C = Q * (2 * K + 1);
+      if (C + 2 * kZmax >= (1ll << 32)) return ADCT_ERR_UNSUPPORTED;
+      int found = -1;
+      uint64_t mw = 0;
+      for (int sh = 0; sh < 16 && found < 0; ++sh) {
+        const uint64_t m = ((1ull << (32 + sh)) + (uint64_t)D - 1) / (uint64_t)D;
+        if (m > 0xFFFFFFFFull) break;
+        bool ok = true;
+        for (int64_t Z = -kZmax; Z <= kZmax; ++Z) {
+          const int64_t U = 2 * Z - (Z < 0 ? 1 : 0) + C;
+          const int64_t got = (int64_t)((((uint64_t)U * m) >> 32) >> sh) - K;
+          if (U < 0 || got != rha_div(Z, Q)) { ok = false; break; }
+        }
+        if (ok) { found = sh; mw = m; }
+      }
+      if (found < 0) return ADCT_ERR_UNSUPPORTED;
+      out->magic_w[p] = (uint32_t)mw;
+      out->cadd_w[p] = (int32_t)C;
+      out->kw[p] = (int32_t)K;
+      out->shift_w[p] = found;
+    }
   }
   // |64 (x_hat - 128)| <= 8192 + max_ij sum_uv |T_ui T_vj| E_uv Q'_uv / 2
   // (exact reconstruction of the level-shifted block is within [-8192, 8128];
@@ -175,17 +240,15 @@ int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out
     for (int j = 0; j < 8; ++j) {
       double s = 0.0;
       for (int u = 0; u < 8; ++u)
-        for (int v = 0; v < 8; ++v) {
-          const int t = t_entry(u, i) * t_entry(v, j);
-          if (t != 0) s += 0.5 * (double)out->qe[u * 8 + v];
-        }
+        for (int v = 0; v < 8; ++v)
+          if (t_entry(u, i) * t_entry(v, j) != 0) s += 0.5 * (double)out->qe[u * 8 + v];
       if (s > worst) worst = s;
     }
   const double bound = 8192.0 + worst;
-  out->max_abs_v = bound > 2.0e9 ? 2000000000 : (int32_t)std::ceil(bound);
-  out->wide = (bound + 32.0 > 32767.0) ? 1 : 0;
-  // The 32-bit path needs |V| + 32 to stay far from int32 overflow.
-  if (bound > 1.0e9) return ADCT_ERR_UNSUPPORTED;
+  if (bound > 1.0e9) return ADCT_ERR_UNSUPPORTED;  // keeps the 32-bit path far from overflow
+  out->max_abs_v = (int32_t)std::ceil(bound);
+  out->wide = (!packed_ok || bound + 32.0 > 32767.0) ? 1 : 0;
+  out->aligned = (!out->wide && bound + 32.0 <= 24576.0) ? 1 : 0;
   out->quality = quality;
   return ADCT_OK;
 }
@@ -332,22 +395,28 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
   if (qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   for (int p = 0; p < 64; ++p)
     if (qtab->qprime[p] < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
+  if (!qtab->wide && qtab->mult[0] == 0) return ADCT_ERR_INVALID_ARGUMENT;  // not built by adct_qtab_*
+  const bool wide = qtab->wide != 0;
   PlaneSetHost ps;
-  int rc = build_planes(planes, n_planes, n_frames, ps);
+  int rc = build_planes(planes, n_planes, n_frames, ps, wide);
   if (rc != ADCT_OK) return rc;
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
-  const QParamsDev q = to_qparams(*qtab);
   u64* d_sse = reinterpret_cast<u64*>(sse);
-  const bool wide = qtab->wide != 0;
+  if (wide) {
+    const QParamsWide qw = to_qparams_wide(*qtab);
+    return for_frame_chunks(ps, n_frames, [&](dim3 g) { k_quant_wide<<<g, kThreads, 0, s>>>(ps.dev, qw, d_sse); });
+  }
+  const QParamsDev q = to_qparams(*qtab);
+  const bool al = qtab->aligned != 0;
   return for_frame_chunks(ps, n_frames, [&](dim3 g) {
     if (ps.pair) {
-      if (wide) k_quant<true, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
-      else k_quant<true, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      if (al) k_quant<true, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      else k_quant<true, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
     } else {
-      if (wide) k_quant<false, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
-      else k_quant<false, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      if (al) k_quant<false, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
+      else k_quant<false, true><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
     }
   });
 }

@@ -1,0 +1,155 @@
+"""C ABI: the library loads on a CPU-only box, exports every symbol declared
+in include/adct_cuda.h, the ctypes prototypes match the header, and the
+host-side logic (quantiser tables, argument validation) behaves.  No CUDA
+compute is called here."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import exact
+from paper_1702_00817_b200 import _lib, errors, quant
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "adct_cuda.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return re.findall(r"^[a-z_0-9 ]+?\**\s*\b(adct_[a-z0-9_]+)\s*\(", src, flags=re.M)
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    names = header_functions()
+    assert len(names) >= 20
+    L = _lib.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    # and the dynamic symbol table really has them (not just ctypes lookup)
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}$", out, flags=re.M), n
+
+
+def test_prototypes_cover_header_exactly():
+    assert set(header_functions()) == set(_lib.PROTOTYPES)
+
+
+def test_struct_sizes_match_header():
+    # adct_qtab_t: 10 x 64 int32 + 4 int32; adct_plane_t: 2 ptr + 2 int32 + 2 int64
+    assert ctypes.sizeof(_lib.QTab) == (10 * 64 + 4) * 4
+    assert ctypes.sizeof(_lib.Plane) == 8 + 8 + 4 + 4 + 8 + 8
+
+
+def test_no_nccl_or_torch_linked():
+    out = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in out and "torch" not in out
+
+
+def test_version_and_strerror():
+    L = _lib.lib()
+    assert L.adct_version() >= 10000
+    assert L.adct_strerror(2).decode() == "retention count must be in [1, 64]"
+    assert L.adct_strerror(999).decode() == "unknown error"
+
+
+def test_sass_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("q", [1, 5, 10, 25, 30, 50, 75, 90, 95, 100])
+def test_qtab_from_quality_matches_oracle(q):
+    t = quant.quant_table(q)
+    assert np.array_equal(quant.qtab_qprime(t), exact.qprime(quant.q50_luma(), q))
+    assert np.array_equal(quant.qtab_qprime(t), quant.qprime_for_quality(q))
+    qe = np.frombuffer(bytes(t.qe), dtype=np.int32).reshape(8, 8)
+    assert np.array_equal(qe, quant.qtab_qprime(t) * exact.E)
+    assert t.quality == q
+
+
+def test_qtab_range_flags():
+    # q >= 25 tables are exact in 16-bit lanes; coarse ones need the 32-bit kernel
+    assert quant.quant_table(10).wide == 1 and quant.quant_table(25).wide == 0
+    assert quant.quant_table(75).aligned == 1 and quant.quant_table(25).aligned == 0
+    t = quant.quant_table(75)
+    # bound: 8192 + max_ij sum_uv |T_ui T_vj| E_uv Q'_uv / 2
+    qe = quant.qtab_qprime(t) * exact.E
+    absT = np.abs(exact.T)
+    b = 8192 + max((absT[:, i][:, None] * absT[:, j][None, :] * qe).sum() / 2 for i in range(8) for j in range(8))
+    assert t.max_abs_v == int(np.ceil(b))
+
+
+def test_qtab_quantiser_constants_are_exact():
+    """Replay the device formulas in numpy over every reachable coefficient."""
+    for q in (25, 50, 75, 90, 100):
+        t = quant.quant_table(q)
+        Qp = quant.qtab_qprime(t).reshape(64)
+        Z = np.arange(-8192, 8193, dtype=np.int64)
+        want = np.sign(Z)[None, :] * ((2 * np.abs(Z)[None, :] + Qp[:, None]) // (2 * Qp[:, None]))
+        mag = np.frombuffer(bytes(t.magic), dtype=np.uint32).astype(np.uint64)
+        bias = np.frombuffer(bytes(t.bias), dtype=np.int32).astype(np.int64)
+        mult = np.frombuffer(bytes(t.mult), dtype=np.int32).astype(np.int64)
+        kq = np.frombuffer(bytes(t.kq), dtype=np.int32).astype(np.int64)
+        U = (Z[None, :] + bias[:, None]) * mult[:, None] + (Z >= 0)[None, :]
+        assert U.min() >= 0 and U.max() <= 0xFFFF
+        got = ((U.astype(np.uint64) * mag[:, None]) >> np.uint64(32)).astype(np.int64) - kq[:, None]
+        assert np.array_equal(got, want), q
+
+
+def test_qtab_build_from_fold_and_errors():
+    from paper_1702_00817_b200 import transforms
+
+    tr = transforms.proposed_transform()
+    qpu = quant.fold_scaling_into_quantization(tr, quant.q50_luma() * 0.5)
+    t = quant.quant_table(qprime_unrounded=qpu)
+    assert np.array_equal(quant.qtab_qprime(t), quant.qtab_qprime(quant.quant_table(75)))
+    assert t.quality == -1
+    bad = qpu.copy()
+    bad[3, 3] = 0.0
+    with pytest.raises(errors.NonPositiveQuantizer):
+        quant.quant_table(qprime_unrounded=bad)
+    with pytest.raises(errors.NonPositiveQuantizer):
+        quant.fold_scaling_into_quantization(tr, -np.ones((8, 8)))
+    with pytest.raises(errors.BadDimensions):
+        quant.fold_scaling_into_quantization(tr, np.ones((4, 4)))
+    with pytest.raises(ValueError):
+        quant.quant_table(0)
+
+
+def test_entry_points_validate_before_any_cuda_call():
+    """Contract errors come back before anything touches the device, so they
+    work on a CPU-only box with null pointers."""
+    L = _lib.lib()
+    n = ctypes.c_void_p(0)
+    assert L.adct_compress_retain(n, n, 1, 64, 64, 4096, 4096, 0, n, n, n) == 2  # InvalidRetention
+    assert L.adct_compress_retain(n, n, 1, 64, 64, 4096, 4096, 65, n, n, n) == 2
+    assert L.adct_compress_retain(n, n, 1, 60, 64, 4096, 4096, 10, n, n, n) == 1  # BadDimensions
+    assert L.adct_compress_retain(n, n, -1, 64, 64, 4096, 4096, 10, n, n, n) == 5
+    assert L.adct_forward_int32(n, 1, 64, 63, 4096, 0, n, n) == 1
+    assert L.adct_sweep_retain_sse(n, 1, 64, 64, 4096, 5, 4, n, n) == 2
+    assert L.adct_inverse_f64(n, 1, 64, 64, 0, 1, n, n) == 2
+    # zero images: nothing to do, no device access
+    assert L.adct_compress_retain(n, n, 0, 64, 64, 4096, 4096, 10, n, n, n) == 0
+    qt = quant.quant_table(50)
+    assert L.adct_compress_quant(n, n, 1, 64, 12, 768, 768, ctypes.byref(qt), n, n) == 1
+    bad = _lib.QTab()
+    assert L.adct_compress_quant(n, n, 1, 64, 64, 4096, 4096, ctypes.byref(bad), n, n) == 3
+    planes = (_lib.Plane * 4)()
+    assert L.adct_compress_quant_planes(planes, 4, 1, ctypes.byref(qt), n, n) == 5
+
+
+def test_error_mapping():
+    with pytest.raises(errors.InvalidRetention):
+        _lib.check(2)
+    with pytest.raises(errors.BadDimensions):
+        _lib.check(1)
+    with pytest.raises(errors.NonPositiveQuantizer):
+        _lib.check(3)
+    with pytest.raises(RuntimeError):
+        _lib.check(7)

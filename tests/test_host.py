@@ -1,0 +1,127 @@
+"""Host-side logic on CPU: transform definitions, reference-mirror API
+validation (errors raised before any device work), sharding arithmetic, the
+numpy mirror of the synthetic generator."""
+
+import numpy as np
+import pytest
+
+from oracle import exact
+from paper_1702_00817_b200 import codec, errors, metrics, shard, synth, transforms
+
+
+def test_transform_from_stages_equals_reference_matrix():
+    t = transforms.proposed_transform()
+    assert np.array_equal(t.kernel.entries, exact.T)
+    assert np.abs(t.matrix @ t.matrix.T - np.eye(8)).max() < 1e-12
+    a1, a2, a3, p = transforms.stage_matrices()
+    assert np.array_equal(p @ a3 @ a2 @ a1, exact.T)
+    assert transforms.is_proposed(t)
+    assert not transforms.is_proposed(transforms.exact_dct_matrix())
+
+
+def test_transform_validation_errors():
+    with pytest.raises(errors.ZeroRow):
+        transforms.TransformMatrix("z", np.zeros((8, 8), dtype=int))
+    with pytest.raises(ValueError):
+        transforms.TransformMatrix("b", np.full((8, 8), 3))
+    bad = transforms.TransformMatrix("b", np.ones((8, 8), dtype=int))
+    with pytest.raises(errors.NonOrthogonalKernel):
+        transforms.ApproximateTransform(bad, transforms.proposed_scaling())
+
+
+def test_dct_is_orthonormal():
+    c = transforms.exact_dct_matrix().matrix
+    assert np.abs(c @ c.T - np.eye(8)).max() < 1e-12
+    assert c[1, 0] == pytest.approx(0.490393, abs=1e-6)
+
+
+def test_zigzag_and_masks():
+    assert codec.ZIGZAG_INDICES == exact.zigzag_indices()
+    assert codec.zigzag_positions()[:3] == ((0, 0), (0, 1), (1, 0))
+    m = codec.retention_mask(10)
+    assert m.sum() == 10 and not m.flags.writeable
+    assert m[:4, :4].sum() == 10  # N8: r = 10 keeps only u, v <= 3
+    b = np.arange(64, dtype=float).reshape(8, 8)
+    assert np.array_equal(codec.retain_coefficients(b, 64), b)
+    assert codec.retain_coefficients(b, 1).sum() == 0.0 and codec.retain_coefficients(b, 1)[0, 0] == 0.0
+    r3 = codec.retain_coefficients(b + 1, 3)
+    assert np.count_nonzero(r3) == 3
+    assert np.array_equal(codec.retain_coefficients(r3, 3), r3)  # idempotent
+    assert codec.compression_ratio(2) == 96.875 and codec.compression_ratio(25) == 60.9375
+
+
+@pytest.mark.parametrize("r", [0, 65, -3])
+def test_invalid_retention_raised_before_compute(r):
+    t = transforms.proposed_transform()
+    img = np.zeros((16, 16), np.uint8)
+    with pytest.raises(errors.InvalidRetention):
+        codec.compress_image(t, img, r)
+    with pytest.raises(errors.InvalidRetention):
+        codec.retention_mask(r)
+    with pytest.raises(errors.InvalidRetention):
+        codec.compression_ratio(r)
+
+
+def test_bad_dimensions_raised_before_compute():
+    t = transforms.proposed_transform()
+    with pytest.raises(errors.BadDimensions):
+        codec.compress_image(t, np.zeros((12, 16)), 10)
+    with pytest.raises(errors.BadDimensions):
+        codec.coefficient_blocks(t, np.zeros((16, 20)))
+    with pytest.raises(errors.BadDimensions):
+        codec.coefficient_blocks(t, np.zeros((2, 16, 16)))
+    with pytest.raises(errors.BadDimensions):
+        codec.retain_coefficients(np.zeros((4, 4)), 3)
+
+
+def test_other_transforms_rejected():
+    with pytest.raises(NotImplementedError):
+        codec.compress_image(transforms.exact_dct_matrix(), np.zeros((8, 8)), 3)
+
+
+def test_metrics_host_functions():
+    assert metrics.psnr(1.0) == pytest.approx(48.13080360867909)
+    assert metrics.psnr(0.0) == float("inf")
+    with pytest.raises(ValueError):
+        metrics.psnr(-1.0)
+    with pytest.raises(errors.DimensionMismatch):
+        metrics.mse(np.zeros((2, 2)), np.zeros((2, 3)))
+    recs = [metrics.QualityRecord("a", "proposed", 10, 4.0, 42.0), metrics.QualityRecord("b", "proposed", 10, 2.0, 44.0)]
+    (s,) = metrics.summarize(recs)
+    assert s.avg_mse == 3.0 and s.avg_psnr == 43.0 and s.n_images == 2
+    (s2,) = metrics.summarize(recs, psnr_from_avg_mse=True)
+    assert s2.avg_psnr == pytest.approx(metrics.psnr(3.0))
+    with pytest.raises(errors.EmptyGroup):
+        metrics.summarize([])
+    assert metrics.ape_vs_dct(1.1, 1.0) == pytest.approx(10.0)
+
+
+@pytest.mark.parametrize("n,world", [(10, 4), (4096, 8), (3, 8), (0, 2), (7, 1)])
+def test_shard_ranges_partition(n, world):
+    parts = [shard.shard_range(n, r, world) for r in range(world)]
+    assert parts[0].start == 0 and parts[-1].stop == n
+    assert all(a.stop == b.start for a, b in zip(parts, parts[1:]))
+    sizes = [p.count for p in parts]
+    assert max(sizes) - min(sizes) <= 1 and sum(sizes) == n
+
+
+def test_synth_numpy_generator_properties():
+    p = synth.blob_params(5, 512, 512, 16, 8.0, 64.0)
+    assert p.shape == (16, 4)
+    assert np.all((p[:, 2] >= 8) & (p[:, 2] <= 64)) and np.all(np.abs(p[:, 3]) <= 80)
+    a = synth.images_np([0, 1], 128, 128, 16, 8.0, 64.0)
+    b = synth.images_np([0, 1], 128, 128, 16, 8.0, 64.0)
+    assert a.dtype == np.uint8 and np.array_equal(a, b) and not np.array_equal(a[0], a[1])
+    z = synth.hash_normal(3, np.arange(200000, dtype=np.uint64))
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+    v = synth.video_blob_params(0, 5, 64, 64, 16, 8.0, 64.0)
+    assert np.array_equal(v[0], synth.video_blob_params(0, 1, 64, 64, 16, 8.0, 64.0)[0])
+    assert np.all(v[1:, :, 2:] == v[:1, :, 2:])  # only centres drift
+
+
+def test_golden_images_reproduce_from_generator():
+    import os
+
+    imgs = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "images.npz")))
+    again = synth.images_np([1], 128, 128, 16, 8.0, 64.0)[0]
+    assert np.mean(again != imgs["c1_seed1_128"]) < 1e-3
