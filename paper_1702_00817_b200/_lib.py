@@ -14,7 +14,9 @@ from ctypes import POINTER, c_double, c_float, c_int, c_int16, c_int32, c_int64,
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libadct_cuda.so")
+LIB_PATH = os.environ.get(
+    "ADCT_LIB_PATH", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libadct_cuda.so")
+)
 
 
 class NativeLibraryError(RuntimeError):

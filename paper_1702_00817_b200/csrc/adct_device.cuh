@@ -308,12 +308,37 @@ __device__ __forceinline__ u32 emit_unit(const u32 (&U)[8][8], const uint4 (&w)[
 }
 
 // Sum of a per-thread u32 partial over the warp (REDUX), one 64-bit atomic
-// per warp.  No CTA barrier: warps that finish early leave immediately.
+// per warp (used where a kernel reduces many times, e.g. the sweep).
 // Per-thread partials are <= 128 * 255^2 < 2^24, per-warp sums < 2^29.
-// All threads of a CTA target the same image/plane (tiles never straddle).
 __device__ __forceinline__ void block_add_u32(u32 v, u64* dst) {
   v = __reduce_add_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0 && v != 0) atomicAdd(dst, (u64)v);
+}
+
+// Per-CTA SSE accumulator without an end-of-kernel barrier or fence: each
+// warp adds (1 << 32) + its REDUX sum to one 64-bit shared word, so the
+// atomic's return value tells the last warp to arrive the CTA total, and
+// that warp issues the CTA's single global 64-bit atomic.  The CTA total is
+// < 256 * 128 * 255^2 < 2^32, so the sum never carries into the count.  All
+// threads of a CTA target the same image/plane (tiles never straddle).
+struct CtaSum {
+  u64 word;  // [63:32] warps arrived, [31:0] partial sum
+};
+
+__device__ __forceinline__ void cta_sum_init(CtaSum& s) {
+  if (threadIdx.x == 0) s.word = 0;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cta_sum_add(CtaSum& s, u32 v, u64* dst) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) {
+    const u64 old = atomicAdd(&s.word, (1ull << 32) | (u64)v);
+    if ((u32)(old >> 32) == kThreads / 32 - 1) {
+      const u64 total = (u64)(u32)old + v;
+      if (total != 0) atomicAdd(dst, total);
+    }
+  }
 }
 
 __device__ __forceinline__ void block_add_u64(u64 v, u64* dst) {

@@ -41,11 +41,14 @@ __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
   return (qa + (qb << 16)) * q.qe[p] + q.wadd[p];
 }
 
+
 // ---------------------------------------------------------------------------
 // K2: fused retain-r, r a template parameter (pruned at compile time).
 // ---------------------------------------------------------------------------
 template <int R, bool PAIR>
 __global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __restrict__ sse) {
+  __shared__ CtaSum cta;
+  cta_sum_init(cta);
   UnitLoc L;
   u32 acc = 0;
   if (locate_unit<PAIR>(ps, L)) {
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __rest
     inv2d(W, U);
     acc = emit_unit<PAIR>(U, w, L.dst, L.width);
   }
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr) cta_sum_add(cta, acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // Runtime-r variant: ragged widths (PAIR=false) and the exact "unrounded"
@@ -71,6 +74,8 @@ __global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __rest
 template <bool PAIR, bool FSSE>
 __global__ void __launch_bounds__(kThreads)
     k_retain_rt(PlaneSetDev ps, int r, u64* __restrict__ sse, u64* __restrict__ ssef) {
+  __shared__ CtaSum cta;
+  cta_sum_init(cta);
   UnitLoc L;
   u32 acc = 0;
   u64 accf = 0;
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
   }
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr) cta_sum_add(cta, acc, sse + L.frame * ps.n_planes + L.plane);
   if (FSSE) block_add_u64(accf, ssef + L.frame * ps.n_planes + L.plane);
 }
 
@@ -152,6 +157,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < 8; ++i) wo[i] = s_orig[i][threadIdx.x];
     acc = emit_unit<PAIR, FLIP>(U, wo, L.dst, L.width);
   }
+  // Per-warp atomics: measured 8% faster than the per-CTA accumulator for
+  // this issue-bound kernel (the memory-bound retain kernels prefer per-CTA).
   if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
