@@ -125,3 +125,16 @@ def test_golden_images_reproduce_from_generator():
     imgs = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "images.npz")))
     again = synth.images_np([1], 128, 128, 16, 8.0, 64.0)[0]
     assert np.mean(again != imgs["c1_seed1_128"]) < 1e-3
+
+
+def test_lane_range_bound_for_every_r():
+    """16-bit output fields are unambiguous for every retain mask."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "range_bounds.py")
+    spec = importlib.util.spec_from_file_location("range_bounds", path)
+    rb = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(rb)
+    worst = max(rb.worst(r) for r in range(1, 65))
+    assert worst == 27136 and worst + 32 <= 32767
