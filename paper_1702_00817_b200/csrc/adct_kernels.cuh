@@ -163,6 +163,129 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// K3, persistent + cp.async pipelined: a fixed grid (2 CTAs per SM) walks the
+// tiles of all frames; while a tile is transformed, the next tile's rows are
+// already in flight into a 2-stage shared-memory ring (cp.async, no register
+// cost).  Each thread only touches its own smem slots, so the ring needs no
+// CTA barrier; cp.async.wait_group is per thread.
+// ---------------------------------------------------------------------------
+struct TileCursor {
+  int plane;
+  int64_t frame;
+  bool active;
+  const uint8_t* src;
+  uint8_t* dst;
+  int32_t width;
+};
+
+template <bool PAIR>
+__device__ __forceinline__ TileCursor tile_unit(const PlaneSetDev& ps, int64_t tile, u32 tiles_per_frame) {
+  TileCursor c;
+  c.frame = tile / tiles_per_frame;
+  const u32 tb = (u32)(tile - c.frame * tiles_per_frame);
+  int p = 0;
+  if (ps.n_planes > 1 && tb >= ps.p[1].cta_begin) p = 1;
+  if (ps.n_planes > 2 && tb >= ps.p[2].cta_begin) p = 2;
+  const PlaneDev& P = ps.p[p];
+  const u32 unit = (tb - P.cta_begin) * kThreads + threadIdx.x;
+  c.plane = p;
+  c.width = P.width;
+  c.active = unit < P.units;
+  if (c.active) {
+    const u32 brow = unit / P.upr;
+    const u32 ucol = unit - brow * P.upr;
+    const int64_t off = (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
+    c.src = P.src + c.frame * P.src_fs + off;
+    c.dst = P.dst ? P.dst + c.frame * P.dst_fs + off : nullptr;
+  } else {
+    c.src = nullptr;
+    c.dst = nullptr;
+  }
+  return c;
+}
+
+template <bool PAIR>
+__device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor& c) {
+  if (!c.active) return;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const u32 sa = (u32)__cvta_generic_to_shared(slot_base + i * kThreads);
+    const uint8_t* g = c.src + (int64_t)i * c.width;
+    if (PAIR)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <bool PAIR, bool FLIP>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
+              int64_t n_tiles, u32 tiles_per_frame) {
+  extern __shared__ uint4 s_ring[];  // [2][8][kThreads]
+  const int64_t stride = gridDim.x;
+  int64_t tile = blockIdx.x;
+  if (tile >= n_tiles) return;
+  TileCursor cur = tile_unit<PAIR>(ps, tile, tiles_per_frame);
+  cp_async_rows<PAIR>(s_ring + threadIdx.x, cur);
+  cp_async_commit();
+  for (int stage = 0; tile < n_tiles; tile += stride, stage ^= 1) {
+    const int64_t nt = tile + stride;
+    TileCursor nxt;
+    nxt.active = false;
+    if (nt < n_tiles) {
+      nxt = tile_unit<PAIR>(ps, nt, tiles_per_frame);
+      cp_async_rows<PAIR>(s_ring + (stage ^ 1) * 8 * kThreads + threadIdx.x, nxt);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    const uint4* rows = s_ring + stage * 8 * kThreads + threadIdx.x;
+    u32 acc = 0;
+    if (cur.active) {
+      uint4 w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        w[i] = rows[i * kThreads];
+        if (!PAIR) w[i].z = w[i].w = 0u;
+      }
+      u32 x[8][8], U[8][8];
+      unpack_unit(w, x);
+      u32 t[8][8], c[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        u32 col[8], Zc[8], Wc[8], cc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+        fwd8(col, Zc);
+        if (v == 0) Zc[0] -= 8192u * 65537u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) Wc[u] = quant_pair(Zc[u], u * 8 + v, q);
+        inv8(Wc, cc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i][v] = cc[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) inv8(c[i], U[i]);
+      uint4 wo[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        wo[i] = rows[i * kThreads];
+        if (!PAIR) wo[i].z = wo[i].w = 0u;
+      }
+      acc = emit_unit<PAIR, FLIP>(U, wo, cur.dst, cur.width);
+    }
+    if (sse != nullptr) block_add_u32(acc, sse + cur.frame * ps.n_planes + cur.plane);
+    cur = nxt;
+    if (nt >= n_tiles) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K7: retain-r sweep — one read and one forward per unit, then for every r in
 // [r_min, r_max] the masked inverse, rounding and SSE, all from registers
 // (replaces the per-r reconstruct_image + mse loop, cli.py:105-113).

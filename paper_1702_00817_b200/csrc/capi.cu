@@ -3,6 +3,7 @@
 // (errors.py:21-33) and happens before anything is enqueued.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -110,6 +111,24 @@ int for_frame_chunks(PlaneSetHost& ps, int64_t n_frames, F&& launch) {
     ADCT_CUDA_TRY(cudaGetLastError());
   }
   return ADCT_OK;
+}
+
+// Persistent kernels: 2 CTAs of 256 threads per SM.
+int persistent_grid(int* grid) {
+  int dev = 0, sms = 0;
+  ADCT_CUDA_TRY(cudaGetDevice(&dev));
+  ADCT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *grid = 2 * sms;
+  return ADCT_OK;
+}
+
+// ADCT_QUANT_KERNEL=grid selects the one-tile-per-CTA quant kernel (A/B).
+bool use_pipelined_quant() {
+  static const bool v = [] {
+    const char* e = std::getenv("ADCT_QUANT_KERNEL");
+    return !(e && std::strcmp(e, "grid") == 0);
+  }();
+  return v;
 }
 
 QParamsDev to_qparams(const adct_qtab_t& t) {
@@ -410,6 +429,29 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
   }
   const QParamsDev q = to_qparams(*qtab);
   const bool al = qtab->aligned != 0;
+  if (use_pipelined_quant() && ps.grid_x > 0 && n_frames > 0) {
+    const int64_t n_tiles = (int64_t)ps.grid_x * n_frames;
+    int grid = 0;
+    int rc2 = persistent_grid(&grid);
+    if (rc2 != ADCT_OK) return rc2;
+    if ((int64_t)grid > n_tiles) grid = (int)n_tiles;
+    ps.dev.frame_base = 0;
+    const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
+#define ADCT_QP(PA, FL)                                                                        \
+  do {                                                                                         \
+    ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL>,                                      \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_quant_p<PA, FL><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x);      \
+  } while (0)
+    if (ps.pair) {
+      if (al) ADCT_QP(true, false); else ADCT_QP(true, true);
+    } else {
+      if (al) ADCT_QP(false, false); else ADCT_QP(false, true);
+    }
+#undef ADCT_QP
+    ADCT_CUDA_TRY(cudaGetLastError());
+    return ADCT_OK;
+  }
   return for_frame_chunks(ps, n_frames, [&](dim3 g) {
     if (ps.pair) {
       if (al) k_quant<true, false><<<g, kThreads, 0, s>>>(ps.dev, q, d_sse);
@@ -551,7 +593,7 @@ struct adct_pipeline {
   cudaStream_t stream[kDepth] = {};
   uint8_t* d_in[kDepth] = {};
   uint8_t* d_out[kDepth] = {};
-  uint64_t* d_sse[kDepth] = {};
+  uint64_t* d_sse = nullptr;  // SSE of a whole call, copied to the host once at the end
   int64_t sse_cap = 0;
 };
 
@@ -562,8 +604,8 @@ void pipeline_free(adct_pipeline* p) {
     if (p->stream[k]) cudaStreamDestroy(p->stream[k]);
     if (p->d_in[k]) cudaFree(p->d_in[k]);
     if (p->d_out[k]) cudaFree(p->d_out[k]);
-    if (p->d_sse[k]) cudaFree(p->d_sse[k]);
   }
+  if (p->d_sse) cudaFree(p->d_sse);
   delete p;
 }
 
@@ -581,10 +623,19 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
     std::memset(host_sse, 0, (size_t)n * sizeof(uint64_t));
     return ADCT_OK;
   }
-  int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
+  const int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
   if (per < 1) return ADCT_ERR_INVALID_ARGUMENT;  // chunk smaller than one image
-  if (per > p->sse_cap) per = p->sse_cap;
   ADCT_CUDA_TRY(cudaSetDevice(p->device));
+  if (n > p->sse_cap) {  // grow the per-call device SSE vector
+    if (p->d_sse) ADCT_CUDA_TRY(cudaFree(p->d_sse));
+    p->d_sse = nullptr;
+    p->sse_cap = 0;
+    ADCT_CUDA_TRY(cudaMalloc(&p->d_sse, (size_t)n * sizeof(uint64_t)));
+    p->sse_cap = n;
+  }
+  // Chunk i goes to stream i % 3: its H2D, kernel and D2H are ordered on that
+  // stream, and the copy engines overlap chunk i's D2H with chunk i+1's H2D.
+  // Nothing in the loop blocks the host (no pageable-memory copies).
   int64_t chunk = 0;
   for (int64_t i0 = 0; i0 < n; i0 += per, ++chunk) {
     const int b = (int)(chunk % adct_pipeline::kDepth);
@@ -595,17 +646,16 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
     uint8_t* drec = host_rec ? p->d_out[b] : nullptr;
     int rc;
     if (kind == 0)
-      rc = adct_compress_retain(p->d_in[b], drec, m, h, w, px, px, r, p->d_sse[b], nullptr, s);
+      rc = adct_compress_retain(p->d_in[b], drec, m, h, w, px, px, r, p->d_sse + i0, nullptr, s);
     else
-      rc = adct_compress_quant(p->d_in[b], drec, m, h, w, px, px, qtab, p->d_sse[b], s);
+      rc = adct_compress_quant(p->d_in[b], drec, m, h, w, px, px, qtab, p->d_sse + i0, s);
     if (rc != ADCT_OK) return rc;
     if (host_rec)
       ADCT_CUDA_TRY(cudaMemcpyAsync(host_rec + i0 * px, p->d_out[b], (size_t)(m * px),
                                     cudaMemcpyDeviceToHost, s));
-    ADCT_CUDA_TRY(cudaMemcpyAsync(host_sse + i0, p->d_sse[b], (size_t)m * sizeof(uint64_t),
-                                  cudaMemcpyDeviceToHost, s));
   }
   for (int k = 0; k < adct_pipeline::kDepth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+  ADCT_CUDA_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return ADCT_OK;
 }
 
@@ -620,13 +670,11 @@ int adct_pipeline_create(int32_t device, size_t chunk_bytes, adct_pipeline_t** o
   if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   p->device = device;
   p->chunk_bytes = (chunk_bytes + 15) / 16 * 16;
-  p->sse_cap = (int64_t)(p->chunk_bytes / 64);
   cudaError_t e = cudaSetDevice(device);
   for (int k = 0; e == cudaSuccess && k < adct_pipeline::kDepth; ++k) {
     e = cudaStreamCreateWithFlags(&p->stream[k], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_in[k], p->chunk_bytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_out[k], p->chunk_bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_sse[k], (size_t)p->sse_cap * sizeof(uint64_t));
   }
   if (e != cudaSuccess) {
     pipeline_free(p);
