@@ -12,7 +12,7 @@ namespace adct {
 // ---------------------------------------------------------------------------
 struct QParamsDev {
   u32 magic[64];  // umulhi(U, magic) == floor(U / divisor), verified exhaustively
-  u32 bpk[64];    // per-position bias B, both lanes (B * 65537)
+  u32 bm[64];     // per-position bias times mult, both lanes: B * mult * 65537
   u32 mult[64];   // 2 (odd Q', divisor 2Q') or 1 (even Q', divisor Q')
   u32 qe[64];     // Q' * E[u][v]
   u32 wadd[64];   // -kq*qe*65537 (+ (O+32)*65537 at DC: rounding, output offset)
@@ -35,12 +35,11 @@ struct QParamsWide {  // scalar quantiser of k_quant_wide
 //   q + kq = umulhi(U, magic)       (exact, adct_qtab_build)
 __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
   const u32 s = ((z >> 15) & 0x10001u) ^ 0x10001u;
-  const u32 U = (z + q.bpk[p]) * q.mult[p] + s;
+  const u32 U = z * q.mult[p] + q.bm[p] + s;
   const u32 qa = __umulhi(U & 0xFFFFu, q.magic[p]);
   const u32 qb = __umulhi(U >> 16, q.magic[p]);
   return (qa + (qb << 16)) * q.qe[p] + q.wadd[p];
 }
-
 
 // ---------------------------------------------------------------------------
 // K2: fused retain-r, r a template parameter (pruned at compile time).

@@ -136,8 +136,8 @@ QParamsDev to_qparams(const adct_qtab_t& t) {
   const uint32_t dc_out = t.aligned ? 24576u : 32768u;  // output-field offset (see pack_row)
   for (int p = 0; p < 64; ++p) {
     q.magic[p] = t.magic[p];
-    q.bpk[p] = (uint32_t)t.bias[p] * 65537u;
     q.mult[p] = (uint32_t)t.mult[p];
+    q.bm[p] = (uint32_t)t.bias[p] * (uint32_t)t.mult[p] * 65537u;
     q.qe[p] = (uint32_t)t.qe[p];
     q.wadd[p] = (uint32_t)0 - (uint32_t)t.kq[p] * (uint32_t)t.qe[p] * 65537u;
   }
