@@ -136,9 +136,10 @@ def _ref_task(args):
     return refport.psnr(m)
 
 
-def cpu_reference_rate(images, r: int, budget_s: float, cores: int):
-    """Gpixel/s of the reference algorithm over full images and/or row strips of
-    `images`, one task per worker, for about `budget_s` seconds."""
+def cpu_reference_rate(images, r, budget_s: float, cores: int, task=None):
+    """Gpixel/s of the reference algorithm over full `images`, one task per
+    worker, for about `budget_s` seconds (task: _ref_task or _ref_quant_task)."""
+    task = task or _ref_task
     import numpy as np
     from concurrent.futures import ProcessPoolExecutor
 
@@ -148,15 +149,28 @@ def cpu_reference_rate(images, r: int, budget_s: float, cores: int):
     with ProcessPoolExecutor(max_workers=cores) as ex:
         # calibrate on one full image per worker
         t0 = time.perf_counter()
-        list(ex.map(_ref_task, [(images[k % len(images)], r) for k in range(cores)]))
+        list(ex.map(task, [(images[k % len(images)], r) for k in range(cores)]))
         t_full = time.perf_counter() - t0
         rounds = max(1, int(budget_s / max(t_full, 1e-3)))
         tasks = [(images[k % len(images)], r) for k in range(cores * rounds)]
         t0 = time.perf_counter()
-        list(ex.map(_ref_task, tasks))
+        list(ex.map(task, tasks))
         dt = time.perf_counter() - t0
     px = len(tasks) * h * w
     return px / dt / 1e9, dict(images=len(tasks), seconds=dt, image_shape=[h, w])
+
+
+def _ref_quant_task(args):
+    """Quantised pipeline composed of the reference's own float64 functions
+    (oracle/refport.quant_float64: forward_2d_unscaled, folded Q', inverse_2d)
+    + round + clamp + mse + psnr; the reference has no quantised driver."""
+    img, qp = args
+    import numpy as np
+
+    from oracle import refport
+
+    rec = np.clip(np.floor(refport.quant_float64(img, qp) + 0.5), 0, 255)
+    return refport.psnr(refport.mse(img, rec))
 
 
 def reference_arm(args) -> None:
@@ -170,11 +184,25 @@ def reference_arm(args) -> None:
         return
     cfg = CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
-    if cfg["kind"] != "retain":
-        print(json.dumps({"impl": "reference", "unavailable": "reference has no quantised pipeline (configs 2/4); use --config 3"}))
-        return
-    h, w, r = cfg["h"], cfg["w"], cfg["r"]
-    nb, smin, smax = cfg["blobs"]
+    if cfg["kind"] == "retain":
+        h, w, r = cfg["h"], cfg["w"], cfg["r"]
+        nb, smin, smax = cfg["blobs"]
+        task = _ref_task
+        what = "oracle/refport.py float64 path (codec.compress_image + metrics.mse/psnr)"
+    else:
+        from oracle import exact
+        from paper_1702_00817_b200.quant import q50_luma
+
+        if cfg["kind"] == "quant":
+            h, w = cfg["h"], cfg["w"]
+            nb, smin, smax = cfg["blobs"]
+            q = cfg["q"][1]
+        else:  # config 4: the Y plane of the video frames carries 2/3 of the pixels
+            h, w, q = 2160, 3840, cfg["q"]
+            nb, smin, smax = synth.CONFIG_BLOBS[4]
+        r = exact.qprime(q50_luma(), q)
+        task = _ref_quant_task
+        what = f"oracle/refport.quant_float64 (reference float64 functions composed, q={q})"
     n_img = min(cores, 16)
     images = [synth.render_np(synth.blob_params(s, h, w, nb, smin, smax), h, w, s) for s in range(n_img)]
     # per-step sample: `rows` rows of one image per worker, sized so the whole run fits ~3 minutes
@@ -184,28 +212,28 @@ def reference_arm(args) -> None:
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     with ProcessPoolExecutor(max_workers=cores) as ex:
         t0 = time.perf_counter()
-        list(ex.map(_ref_task, [(images[k % n_img], r) for k in range(cores)]))
+        list(ex.map(task, [(images[k % n_img], r) for k in range(cores)]))
         t_full = time.perf_counter() - t0
         rows = int(h * min(1.0, budget_step / max(t_full, 1e-3)))
         rows = max(8, rows - rows % 8)
         strips = [(images[k % n_img][:rows], r) for k in range(cores)]
         for _ in range(args.warmup):
-            list(ex.map(_ref_task, strips))
+            list(ex.map(task, strips))
         times = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            list(ex.map(_ref_task, strips))
+            list(ex.map(task, strips))
             times.append(time.perf_counter() - t0)
     px_step = cores * rows * w
     total = sum(times)
     value = px_step * len(times) / total / 1e9
-    sample = f"{cores} x ({rows}x{w}) strips of config-3 images per step (one per core), oracle/refport.py float64 path"
+    sample = f"{cores} x ({rows}x{w}) strips of config-{args.config} images per step (one per core), {what}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian blobs + N(0,4^2) noise, BASELINE.json generator)",
-        "config": {"workload": cfg["workload"], "r": r},
+        "config": {"workload": cfg["workload"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -356,14 +384,24 @@ def gpu_arm(args) -> None:
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and cfg["kind"] == "retain":
+    if rank == 0 and world == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
-        sample_imgs = [imgs[k].cpu().numpy() for k in range(min(per, 8))]
-        v, info = cpu_reference_rate(sample_imgs, cfg["r"], args.cpu_seconds, cores)
+        if cfg["kind"] == "retain":
+            sample_imgs = [imgs[k].cpu().numpy() for k in range(min(per, 8))]
+            v, info = cpu_reference_rate(sample_imgs, cfg["r"], args.cpu_seconds, cores)
+            algo = "oracle/refport.py = reference codec.compress_image + metrics.mse/psnr float64 algorithm"
+        else:
+            from oracle import exact
+
+            q = cfg["q"][1] if cfg["kind"] == "quant" else cfg["q"]
+            src = imgs if cfg["kind"] == "quant" else planes[0]
+            sample_imgs = [src[k].cpu().numpy() for k in range(min(per, 4))]
+            v, info = cpu_reference_rate(sample_imgs, exact.qprime(quant.q50_luma(), q), args.cpu_seconds, cores,
+                                         task=_ref_quant_task)
+            algo = f"oracle/refport.quant_float64 = reference float64 functions composed (q={q})"
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{info['images']} full {info['image_shape'][0]}x{info['image_shape'][1]} config-3 images, "
-                         f"one per task on {cores} processes, {info['seconds']:.1f}s; oracle/refport.py = reference "
-                         f"codec.compress_image + metrics.mse/psnr float64 algorithm"}
+               "sample": f"{info['images']} full {info['image_shape'][0]}x{info['image_shape'][1]} config-{args.config} images, "
+                         f"one per task on {cores} processes, {info['seconds']:.1f}s; {algo}"}
 
     if rank == 0:
         line = {
