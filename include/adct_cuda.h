@@ -163,10 +163,30 @@ int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes,
  * K7 — retain-r sweep: one read of each image, SSE for every r in
  * [r_min, r_max].  Replaces the per-r loop of cli.run_sweep
  * (cli.py:101-113: reconstruct_image + mse per r).
- * sse: device uint64 [n][r_max - r_min + 1]. */
+ * sse:           device uint64 [n][r_max - r_min + 1], rounded reconstructions
+ * sse_unrounded: device uint64 [n][r_max - r_min + 1], nullable; 4096 x the
+ *                reference's own unrounded clamped SSE (exact). */
 int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w,
                           int64_t img_stride, int32_t r_min, int32_t r_max,
-                          uint64_t* sse, void* stream);
+                          uint64_t* sse, uint64_t* sse_unrounded, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Dense 8x8 transforms in float64 for any 8x8 matrix C (SURVEY §8f row f1:
+ * the exact DCT, kernels.py:166-178, and the registry's comparison kernels,
+ * kernels.py:228-327).  `C` is a HOST pointer to 64 float64 (row-major, the
+ * transform's .matrix), passed to the kernel by value.  Images are uint8
+ * (img_is_f64 == 0) or float64 (img_is_f64 != 0), like the reference's
+ * float64 samples.
+ *   adct_forward_dense:  coef = C X C^T per block (coefficient_blocks, codec.py:120-131)
+ *   adct_inverse_dense:  out = clamp?(untile(C^T mask_r(coef) C))  (reconstruct_image, codec.py:134-141)
+ *   adct_sweep_dense:    sse[n][r] = sum (x - clamp(C^T mask_r(C X C^T) C, 0, 255))^2,
+ *                        float64, every r in [r_min, r_max] (cli.py:105-113). */
+int adct_forward_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, int32_t w,
+                       const double* C, double* coef, void* stream);
+int adct_inverse_dense(const double* coef, int64_t n, int32_t h, int32_t w, const double* C,
+                       int32_t r, int32_t clamp, double* out, void* stream);
+int adct_sweep_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, int32_t w,
+                     const double* C, int32_t r_min, int32_t r_max, double* sse, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Real-valued (float64) transforms, for the reference's float API on

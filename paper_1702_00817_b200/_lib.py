@@ -77,7 +77,19 @@ PROTOTYPES = {
     ),
     "adct_compress_quant_planes": (c_int, [POINTER(Plane), c_int32, c_int64, POINTER(QTab), c_void_p, c_void_p]),
     "adct_compress_retain_planes": (c_int, [POINTER(Plane), c_int32, c_int64, c_int32, c_void_p, c_void_p]),
-    "adct_sweep_retain_sse": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    "adct_sweep_retain_sse": (
+        c_int,
+        [c_void_p, c_int64, c_int32, c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p],
+    ),
+    "adct_forward_dense": (c_int, [c_void_p, c_int32, c_int64, c_int32, c_int32, POINTER(c_double), c_void_p, c_void_p]),
+    "adct_inverse_dense": (
+        c_int,
+        [c_void_p, c_int64, c_int32, c_int32, POINTER(c_double), c_int32, c_int32, c_void_p, c_void_p],
+    ),
+    "adct_sweep_dense": (
+        c_int,
+        [c_void_p, c_int32, c_int64, c_int32, c_int32, POINTER(c_double), c_int32, c_int32, c_void_p, c_void_p],
+    ),
     "adct_forward_f64": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "adct_inverse_f64": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "adct_sse_u8": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p]),

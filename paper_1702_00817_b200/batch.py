@@ -166,7 +166,8 @@ def sweep_retain_sse(images: torch.Tensor, r_min: int = 1, r_max: int = 45) -> t
     images = _as_batch(images)
     n, h, w = images.shape
     sse = torch.empty((n, r_max - r_min + 1), dtype=torch.int64, device=images.device)
-    _lib.call("adct_sweep_retain_sse", _ptr(images), n, h, w, _img_stride(images), r_min, r_max, _ptr(sse), _stream())
+    _lib.call("adct_sweep_retain_sse", _ptr(images), n, h, w, _img_stride(images), r_min, r_max, _ptr(sse), None,
+              _stream())
     return sse
 
 
@@ -220,3 +221,72 @@ def psnr_from_sse(sse, n_pixels: int, *, scale: float = 1.0) -> np.ndarray:
     mse = s / (scale * float(n_pixels))
     with np.errstate(divide="ignore"):
         return np.where(mse == 0, np.inf, 10.0 * np.log10(255.0**2 / np.where(mse == 0, 1.0, mse)))
+
+
+# --- dense float64 transforms for any 8x8 matrix (exact DCT, registry kernels) ---
+
+def _cmat(C) -> "ctypes.Array":
+    a = np.ascontiguousarray(np.asarray(C, dtype=np.float64).reshape(64))
+    if a.size != 64:
+        raise BadDimensions("transform matrix must be 8x8")
+    return (ctypes.c_double * 64)(*a.tolist())
+
+
+def _f64_or_u8(images: torch.Tensor):
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    if images.dim() != 3:
+        raise BadDimensions(f"expected (N, H, W), got {tuple(images.shape)}")
+    n, h, w = images.shape
+    if h % 8 or w % 8:
+        raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+    if images.dtype == torch.uint8:
+        return images.contiguous(), 0
+    return images.to(torch.float64).contiguous(), 1
+
+
+def forward_dense(images: torch.Tensor, C) -> torch.Tensor:
+    """Y = C X C^T per block for any 8x8 C, float64 (coefficient_blocks, codec.py:120-131)."""
+    x, f64 = _f64_or_u8(images)
+    n, h, w = x.shape
+    coef = torch.empty((n, (h // 8) * (w // 8), 8, 8), dtype=torch.float64, device=x.device)
+    _lib.call("adct_forward_dense", _ptr(x), f64, n, h, w, _cmat(C), _ptr(coef), _stream())
+    return coef
+
+
+def inverse_dense(coef: torch.Tensor, h: int, w: int, C, *, r: int = 64, clamp: bool = False) -> torch.Tensor:
+    """untile(C^T mask_r(Y) C), optionally clamped (reconstruct_image, codec.py:134-141)."""
+    if not 1 <= int(r) <= 64:
+        raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+    if h % 8 or w % 8:
+        raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+    nb = (h // 8) * (w // 8)
+    c = coef.to(torch.float64).contiguous()
+    n = c.numel() // (64 * nb) if nb else 0
+    out = torch.empty((n, h, w), dtype=torch.float64, device=c.device)
+    _lib.call("adct_inverse_dense", _ptr(c), n, h, w, _cmat(C), int(r), int(clamp), _ptr(out), _stream())
+    return out
+
+
+def sweep_dense_sse(images: torch.Tensor, C, r_min: int, r_max: int) -> torch.Tensor:
+    """float64 SSE[N, r] of the reference's unrounded, clamped reconstructions for any C."""
+    if not (1 <= r_min <= r_max <= 64):
+        raise InvalidRetention(f"retention range must satisfy 1 <= r_min <= r_max <= 64, got {r_min}..{r_max}")
+    x, f64 = _f64_or_u8(images)
+    n, h, w = x.shape
+    sse = torch.empty((n, r_max - r_min + 1), dtype=torch.float64, device=x.device)
+    _lib.call("adct_sweep_dense", _ptr(x), f64, n, h, w, _cmat(C), r_min, r_max, _ptr(sse), _stream())
+    return sse
+
+
+def sweep_retain_sse_unrounded(images: torch.Tensor, r_min: int = 1, r_max: int = 45):
+    """(rounded SSE, 4096 x unrounded SSE), both int64[N, r] — exact."""
+    if not (1 <= r_min <= r_max <= 64):
+        raise InvalidRetention(f"retention range must satisfy 1 <= r_min <= r_max <= 64, got {r_min}..{r_max}")
+    images = _as_batch(images)
+    n, h, w = images.shape
+    sse = torch.empty((n, r_max - r_min + 1), dtype=torch.int64, device=images.device)
+    ssef = torch.empty_like(sse)
+    _lib.call("adct_sweep_retain_sse", _ptr(images), n, h, w, _img_stride(images), r_min, r_max, _ptr(sse),
+              _ptr(ssef), _stream())
+    return sse, ssef

@@ -14,8 +14,9 @@ Routing:
   float64 matmuls to ~1e-13).
 * The batched, rounded uint8 hot path is `batch.compress_retain` /
   `batch.compress_quant` (exact integer pipeline).
-Only the proposed transform has GPU kernels; other `Transform`s raise
-NotImplementedError (comparison kernels are out of scope).
+Any other `Transform` (the exact DCT, the reference registry's comparison
+kernels — anything with an 8x8 `.matrix`) runs on the dense float64 8x8
+kernels (adct_*_dense).
 """
 
 from __future__ import annotations
@@ -105,11 +106,11 @@ def _back(t: torch.Tensor, to_numpy: bool):
     return t
 
 
-def _require_proposed(t) -> None:
-    if not is_proposed(t):
-        raise NotImplementedError(
-            f"GPU kernels implement the proposed transform only, got {getattr(t, 'name', t)!r}"
-        )
+def _matrix(t) -> np.ndarray:
+    m = np.asarray(getattr(t, "matrix"), dtype=np.float64)
+    if m.shape != (8, 8):
+        raise BadDimensions(f"transform matrix must be 8x8, got {m.shape}")
+    return m
 
 
 def _is_u8_range_integral(a) -> bool:
@@ -142,17 +143,22 @@ def _blocks_as_images(block) -> tuple[object, tuple]:
 
 def forward_2d(t, block):
     """C B C^T (codec.py:68-71), float64, over (..., 8, 8)."""
-    _require_proposed(t)
     x, was_np = _to_dev(block, torch.float64)
     xs, lead = _blocks_as_images(x)
-    y = batch.forward_f64(xs).reshape(*lead, 8, 8) if lead else batch.forward_f64(xs).reshape(8, 8)
-    return _back(y, was_np)
+    y = batch.forward_f64(xs) if is_proposed(t) else batch.forward_dense(xs, _matrix(t))
+    return _back(y.reshape(*lead, 8, 8) if lead else y.reshape(8, 8), was_np)
 
 
 def forward_2d_unscaled(t, block):
     """K B K^T without the diagonal scaling (codec.py:74-81); integer-exact."""
-    _require_proposed(t)
     integral_in = (block.dtype.kind in "iub") if not isinstance(block, torch.Tensor) else not block.dtype.is_floating_point
+    if not is_proposed(t):
+        k = np.asarray(t.kernel.entries, dtype=np.float64)
+        x, was_np = _to_dev(block, torch.float64)
+        xs, lead = _blocks_as_images(x)
+        z = batch.forward_dense(xs, k)
+        z = z.reshape(*lead, 8, 8) if lead else z.reshape(8, 8)
+        return _back(torch.round(z).to(torch.int64) if integral_in else z, was_np)
     if _is_u8_range_integral(block):
         x, was_np = _to_dev(block, torch.uint8)
         xs, lead = _blocks_as_images(x)
@@ -179,32 +185,36 @@ def _d_outer() -> np.ndarray:
 
 def inverse_2d(t, coeffs):
     """C^T Y C (codec.py:84-87), float64, over (..., 8, 8)."""
-    _require_proposed(t)
     y, was_np = _to_dev(coeffs, torch.float64)
     ys, lead = _blocks_as_images(y)
-    x = batch.inverse_f64(ys.reshape(-1, 1, 8, 8), 8, 8, r=64, clamp=False)
+    if is_proposed(t):
+        x = batch.inverse_f64(ys.reshape(-1, 1, 8, 8), 8, 8, r=64, clamp=False)
+    else:
+        x = batch.inverse_dense(ys.reshape(-1, 1, 8, 8), 8, 8, _matrix(t), r=64, clamp=False)
     x = x.reshape(*lead, 8, 8) if lead else x.reshape(8, 8)
     return _back(x, was_np)
 
 
 def coefficient_blocks(t, image):
     """Forward-transform every 8x8 tile; (n_blocks, 8, 8) float64 in raster block order (codec.py:120-131)."""
-    _require_proposed(t)
     shape = tuple(image.shape)
     if len(shape) != 2 or shape[0] % 8 or shape[1] % 8:
         raise BadDimensions(f"image dimensions must be divisible by 8, got {shape}")
     x, was_np = _to_dev(image, torch.float64)
-    c = batch.forward_f64(x.unsqueeze(0))[0]
-    return _back(c, was_np)
+    c = batch.forward_f64(x.unsqueeze(0)) if is_proposed(t) else batch.forward_dense(x.unsqueeze(0), _matrix(t))
+    return _back(c[0], was_np)
 
 
 def reconstruct_image(t, coeffs, r: int, height: int, width: int):
     """Inverse of the first r zigzag coefficients, untiled and clamped to [0,255] (codec.py:134-141)."""
-    _require_proposed(t)
     if not 1 <= r <= 64:
         raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
     c, was_np = _to_dev(coeffs, torch.float64)
-    out = batch.inverse_f64(c.reshape(1, -1, 8, 8), int(height), int(width), r=int(r), clamp=True)[0]
+    c = c.reshape(1, -1, 8, 8)
+    if is_proposed(t):
+        out = batch.inverse_f64(c, int(height), int(width), r=int(r), clamp=True)[0]
+    else:
+        out = batch.inverse_dense(c, int(height), int(width), _matrix(t), r=int(r), clamp=True)[0]
     return _back(out, was_np)
 
 
@@ -212,11 +222,15 @@ def compress_image(t, image, r: int):
     """Forward, keep r zigzag coefficients, inverse, clamp (codec.py:144-155); float64, unrounded."""
     if not 1 <= r <= 64:
         raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
-    _require_proposed(t)
     shape = tuple(image.shape)
     if len(shape) != 2 or shape[0] % 8 or shape[1] % 8:
         raise BadDimensions(f"image dimensions must be divisible by 8, got {shape}")
+    m = None if is_proposed(t) else _matrix(t)
     x, was_np = _to_dev(image, torch.float64)
-    c = batch.forward_f64(x.unsqueeze(0))
-    out = batch.inverse_f64(c, shape[0], shape[1], r=int(r), clamp=True)[0]
+    if m is None:
+        c = batch.forward_f64(x.unsqueeze(0))
+        out = batch.inverse_f64(c, shape[0], shape[1], r=int(r), clamp=True)[0]
+    else:
+        c = batch.forward_dense(x.unsqueeze(0), m)
+        out = batch.inverse_dense(c, shape[0], shape[1], m, r=int(r), clamp=True)[0]
     return _back(out, was_np)

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // ---------------------------------------------------------------------------
 template <bool PAIR>
 __global__ void __launch_bounds__(kThreads)
-    k_sweep(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse) {
+    k_sweep(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse, u64* __restrict__ ssef) {
   UnitLoc L;
   const bool active = locate_unit<PAIR>(ps, L);
   uint4 w[8];
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll 1
   for (int r = r_min; r <= r_max; ++r) {
     u32 acc = 0;
+    u64 accf = 0;
     if (active) {
       u32 W[8][8], U[8][8];
 #pragma unroll
@@ -338,8 +339,28 @@ __global__ void __launch_bounds__(kThreads)
           acc = sse4(w[i].w, o.w, acc);
         }
       }
+      if (ssef != nullptr) {
+        // the reference's unrounded convention: sum (64 x - clamp(64 x_hat, 0, 16320))^2
+        u32 x[8][8];
+        unpack_unit(w, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const u32 c = __vmaxu2(__vminu2(U[i][j], 0x9FE09FE0u), 0x60206020u);
+            const u32 d = (x[i][j] << 6) + 0x60206020u - c;
+            const int da = (int)(d << 16) >> 16;
+            const int db = (int)(d - (u32)da) >> 16;
+            accf += (u64)(da * da) + (PAIR ? (u64)(db * db) : 0ull);
+          }
+      }
     }
     block_add_u32(acc, out + (r - r_min));
+    if (ssef != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) accf += __shfl_xor_sync(0xffffffffu, accf, o);
+      if ((threadIdx.x & 31) == 0 && accf != 0) atomicAdd(ssef + L.frame * nr + (r - r_min), accf);
+    }
   }
 }
 
@@ -552,6 +573,189 @@ __global__ void __launch_bounds__(kThreads)
   }
   // per-thread partial may exceed 2^24 for huge frames: reduce in 64 bits
   block_add_u64((u64)acc, sse + frame);
+}
+
+// ---------------------------------------------------------------------------
+// Dense 8x8 transforms in float64 for any matrix C (the exact DCT and the
+// reference's registry kernels): forward Y = C X C^T,
+// inverse X = C^T mask_r(Y) C (the reference's transpose inverse,
+// codec.py:84-87, also used for flagged non-orthogonal kernels), and an
+// r-sweep that reconstructs incrementally:
+//   x_hat_r = x_hat_{r-1} + Y[u][v] * C[u]^T C[v]   ((u,v) = zigzag position r-1)
+// with the clamped float64 SSE of the reference's convention per r
+// (cli.py:105-113: reconstruct_image + mse).
+// ---------------------------------------------------------------------------
+struct DenseMat {
+  double c[64];  // row-major C[u][k]
+};
+
+__device__ __forceinline__ void dense8(const DenseMat& M, const double (&x)[8], double (&y)[8]) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a = fma(M.c[u * 8 + k], x[k], a);
+    y[u] = a;
+  }
+}
+
+__device__ __forceinline__ void dense8t(const DenseMat& M, const double (&y)[8], double (&x)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    double a = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a = fma(M.c[u * 8 + k], y[u], a);
+    x[k] = a;
+  }
+}
+
+template <typename InT>
+__device__ __forceinline__ void load_block_f64(const InT* src, int w, double (&x)[8][8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[i][j] = (double)src[(int64_t)i * w + j];
+}
+
+// Y = C X C^T: rows then columns.
+__device__ __forceinline__ void dense_fwd2d(const DenseMat& M, const double (&x)[8][8], double (&Y)[8][8]) {
+  double t[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dense8(M, x[i], t[i]);
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    double col[8], out[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+    dense8(M, col, out);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) Y[u][v] = out[u];
+  }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kThreads)
+    k_dense_forward(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M,
+                    double* __restrict__ coef) {
+  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blk >= nblocks) return;
+  const int64_t frame = blockIdx.y;
+  const int nbc = w / 8;
+  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
+  double x[8][8], Y[8][8];
+  load_block_f64(img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8, w, x);
+  dense_fwd2d(M, x, Y);
+  double* dst = coef + (frame * nblocks + blk) * 64;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) dst[u * 8 + v] = Y[u][v];
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_dense_inverse(const double* __restrict__ coef, int h, int w, int64_t nblocks, int r, int clamp,
+                    const DenseMat M, double* __restrict__ out) {
+  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (blk >= nblocks) return;
+  const int64_t frame = blockIdx.y;
+  const int nbc = w / 8;
+  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
+  const double* src = coef + (frame * nblocks + blk) * 64;
+  double Y[8][8], c[8][8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) Y[u][v] = (zz_rank(u, v) < r) ? src[u * 8 + v] : 0.0;
+  // columns: c[:, v] = C^T Y[:, v]; rows: x[i, :] = C^T c[i, :]
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    double col[8], o[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) col[u] = Y[u][v];
+    dense8t(M, col, o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][v] = o[i];
+  }
+  double* dst = out + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double o[8];
+    dense8t(M, c[i], o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[(int64_t)i * w + j] = clamp ? fmin(fmax(o[j], 0.0), 255.0) : o[j];
+  }
+}
+
+// One thread per block; per r a block-wide float64 sum and one atomic per CTA.
+template <typename InT>
+__global__ void __launch_bounds__(kThreads)
+    k_dense_sweep(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M, int r_min,
+                  int r_max, double* __restrict__ sse) {
+  __shared__ double red[kThreads / 32];
+  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool active = blk < nblocks;
+  const int64_t frame = blockIdx.y;
+  const int nbc = w / 8;
+  double x[8][8], Y[8][8], V[8][8];
+  if (active) {
+    const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
+    load_block_f64(img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8, w, x);
+    dense_fwd2d(M, x, Y);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[i][j] = Y[i][j] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) V[i][j] = 0.0;
+  const int nr = r_max - r_min + 1;
+#pragma unroll 1
+  for (int k = 0; k < r_max; ++k) {
+    // zigzag position of rank k (uniform across the CTA)
+    int pos = 0;
+#pragma unroll
+    for (int p = 0; p < 64; ++p)
+      if (zz_rank(p >> 3, p & 7) == k) pos = p;
+    const int u = pos >> 3, v = pos & 7;
+    double y = 0.0;
+#pragma unroll
+    for (int uu = 0; uu < 8; ++uu)
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv)
+        if (uu == u && vv == v) y = Y[uu][vv];
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = y * M.c[u * 8 + i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) V[i][j] = fma(a[i], M.c[v * 8 + j], V[i][j]);
+    if (k + 1 < r_min) continue;
+    double acc = 0.0;
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double d = x[i][j] - fmin(fmax(V[i][j], 0.0), 255.0);
+          acc = fma(d, d, acc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kThreads / 32; ++q) t += red[q];
+      atomicAdd(sse + frame * nr + (k + 1 - r_min), t);
+    }
+    __syncthreads();
+  }
 }
 
 #endif  // ADCT_DEFINE_PLAIN_KERNELS

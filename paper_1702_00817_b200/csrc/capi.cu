@@ -473,7 +473,8 @@ int adct_compress_quant(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h, 
 
 // --- K7 sweep ----------------------------------------------------------------
 int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, int64_t img_stride,
-                          int32_t r_min, int32_t r_max, uint64_t* sse, void* stream) {
+                          int32_t r_min, int32_t r_max, uint64_t* sse, uint64_t* sse_unrounded,
+                          void* stream) {
   if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
   if (r_min < 1 || r_max > 64 || r_min > r_max) return ADCT_ERR_INVALID_RETENTION;
   adct_plane_t pl = single_plane(img, nullptr, h, w, img_stride, 0);
@@ -484,10 +485,12 @@ int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, i
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n * (size_t)(r_max - r_min + 1);
   if (nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
+  if (nsse && sse_unrounded) ADCT_CUDA_TRY(cudaMemsetAsync(sse_unrounded, 0, nsse * sizeof(uint64_t), s));
   u64* d_sse = reinterpret_cast<u64*>(sse);
+  u64* d_ssef = reinterpret_cast<u64*>(sse_unrounded);
   return for_frame_chunks(ps, n, [&](dim3 g) {
-    if (ps.pair) k_sweep<true><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse);
-    else k_sweep<false><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse);
+    if (ps.pair) k_sweep<true><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse, d_ssef);
+    else k_sweep<false><<<g, kThreads, 0, s>>>(ps.dev, r_min, r_max, d_sse, d_ssef);
   });
 }
 
@@ -532,6 +535,92 @@ int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w, int32_
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
     k_inverse_f64<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r,
                                                                clamp, out + f0 * (int64_t)h * w);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+// --- dense float64 transforms (exact DCT, registry kernels) -----------------
+static int dense_setup(const double* C, DenseMat& M) {
+  if (C == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  for (int k = 0; k < 64; ++k) {
+    if (!std::isfinite(C[k])) return ADCT_ERR_INVALID_ARGUMENT;
+    M.c[k] = C[k];
+  }
+  return ADCT_OK;
+}
+
+int adct_forward_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, int32_t w,
+                       const double* C, double* coef, void* stream) {
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  DenseMat M;
+  if ((rc = dense_setup(C, M)) != ADCT_OK) return rc;
+  if (n == 0 || nb == 0) return ADCT_OK;
+  if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    const dim3 g(gx, (unsigned)nf);
+    if (img_is_f64)
+      k_dense_forward<double><<<g, kThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M,
+                                                      coef + f0 * nb * 64);
+    else
+      k_dense_forward<uint8_t><<<g, kThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
+                                                       coef + f0 * nb * 64);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+int adct_inverse_dense(const double* coef, int64_t n, int32_t h, int32_t w, const double* C, int32_t r,
+                       int32_t clamp, double* out, void* stream) {
+  if (r < 1 || r > 64) return ADCT_ERR_INVALID_RETENTION;
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  DenseMat M;
+  if ((rc = dense_setup(C, M)) != ADCT_OK) return rc;
+  if (n == 0 || nb == 0) return ADCT_OK;
+  if (coef == nullptr || out == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    k_dense_inverse<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r, clamp, M,
+                                                               out + f0 * (int64_t)h * w);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
+int adct_sweep_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, int32_t w, const double* C,
+                     int32_t r_min, int32_t r_max, double* sse, void* stream) {
+  if (r_min < 1 || r_max > 64 || r_min > r_max) return ADCT_ERR_INVALID_RETENTION;
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  DenseMat M;
+  if ((rc = dense_setup(C, M)) != ADCT_OK) return rc;
+  if (n == 0) return ADCT_OK;
+  if (sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const int nr = r_max - r_min + 1;
+  ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, (size_t)n * nr * sizeof(double), s));
+  if (nb == 0) return ADCT_OK;
+  if (img == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    const dim3 g(gx, (unsigned)nf);
+    if (img_is_f64)
+      k_dense_sweep<double><<<g, kThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M, r_min,
+                                                    r_max, sse + f0 * nr);
+    else
+      k_dense_sweep<uint8_t><<<g, kThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
+                                                     r_min, r_max, sse + f0 * nr);
     ADCT_CUDA_TRY(cudaGetLastError());
   }
   return ADCT_OK;

@@ -1,0 +1,160 @@
+"""GPU-backed corpus sweep — the reference's caller of the hot path re-pointed
+at the batch kernels (reference cli.py:53-152).
+
+`run_sweep` keeps the reference's contract: for every (transform, image, r)
+it records the MSE and PSNR of the *unrounded, clamped* reconstruction
+(codec.reconstruct_image + metrics.mse, cli.py:105-113), then summarises per
+(transform, r) and computes the APE of the average MSE against the exact DCT.
+The loop over images and r is replaced by one launch per image batch:
+
+* "proposed": `adct_sweep_retain_sse` — one read per image, exact integer
+  SSE for every r (the unrounded SSE is 4096 x the reference's, exactly);
+* any other transform ("dct", or a registry transform object with an 8x8
+  `.matrix`): `adct_sweep_dense` — float64, incremental per r.
+
+`write_sweep_outputs` writes records.csv, summary.csv and run_metadata.json in
+the reference's format (cli.py:127-152, metrics.py:100-122).
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+import math
+from dataclasses import asdict, dataclass
+from pathlib import Path
+from typing import Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import batch, codec, metrics, transforms
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """Mirror of cli.ExperimentConfig (cli.py:53-73); `transforms` holds names
+    ("dct", "proposed") or transform objects (e.g. registry kernels)."""
+
+    transforms: tuple
+    r_min: int = 2
+    r_max: int = 45
+    corpus_path: str | None = None
+    seed: int = 2012
+    n_images: int = 45
+    psnr_from_avg_mse: bool = False
+
+    def __post_init__(self) -> None:
+        if not self.transforms:
+            raise ValueError("at least one transform is required")
+        if not (1 <= self.r_min <= self.r_max <= 64):
+            raise ValueError(f"retention range [{self.r_min}, {self.r_max}] not within [1, 64]")
+
+    @property
+    def r_values(self) -> range:
+        return range(self.r_min, self.r_max + 1)
+
+
+def resolve_transform(t):
+    """Name -> transform for the built-ins (cli.py:40-50); objects pass through."""
+    if isinstance(t, str):
+        if t == "dct":
+            return transforms.exact_dct_matrix()
+        if t == "proposed":
+            return transforms.proposed_transform()
+        raise ValueError(f"unknown transform {t!r}; pass registry transforms as objects")
+    return t
+
+
+def _name(t) -> str:
+    return t if isinstance(t, str) else t.name
+
+
+def _group_by_shape(images):
+    groups: dict[tuple, list[int]] = {}
+    for k, (_, s) in enumerate(images):
+        groups.setdefault((tuple(np.shape(s)), np.asarray(s).dtype.kind), []).append(k)
+    return groups
+
+
+def _is_u8_exact(arr: np.ndarray) -> bool:
+    return arr.dtype == np.uint8 or (
+        arr.dtype.kind in "fiu" and bool(np.all((arr >= 0) & (arr <= 255) & (arr == np.round(arr))))
+    )
+
+
+def sweep_mse(t, stack: np.ndarray, r_min: int, r_max: int, device=None) -> np.ndarray:
+    """MSE[N, r] of the unrounded clamped reconstructions of an (N, H, W) stack."""
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    n, h, w = stack.shape
+    tr = resolve_transform(t)
+    if transforms.is_proposed(tr) and _is_u8_exact(stack):
+        x = torch.from_numpy(np.ascontiguousarray(stack.astype(np.uint8))).to(dev)
+        _, ssef = batch.sweep_retain_sse_unrounded(x, r_min, r_max)
+        torch.cuda.current_stream().synchronize()
+        return ssef.cpu().numpy().astype(np.float64) / (4096.0 * h * w)
+    x = torch.from_numpy(np.ascontiguousarray(stack)).to(dev)
+    if x.dtype != torch.uint8:
+        x = x.to(torch.float64)
+    sse = batch.sweep_dense_sse(x, np.asarray(tr.matrix, dtype=np.float64), r_min, r_max)
+    torch.cuda.current_stream().synchronize()
+    return sse.cpu().numpy() / float(h * w)
+
+
+def run_sweep(config: ExperimentConfig, images: Sequence[tuple[str, np.ndarray]]):
+    """(records, summaries, ape) exactly as cli.run_sweep (cli.py:87-124) returns them.
+
+    `images` are (image_id, samples) pairs (the reference's PGM and synthetic
+    corpus loaders are out of scope; pass arrays)."""
+    records: list[metrics.QualityRecord] = []
+    groups = _group_by_shape(images)
+    for t in config.transforms:
+        name = _name(t)
+        per_image: dict[int, np.ndarray] = {}
+        for _, idx in groups.items():
+            stack = np.stack([np.asarray(images[k][1]) for k in idx])
+            m = sweep_mse(t, stack, config.r_min, config.r_max)
+            for row, k in enumerate(idx):
+                per_image[k] = m[row]
+        for k, (image_id, _) in enumerate(images):
+            for j, r in enumerate(config.r_values):
+                err = float(per_image[k][j])
+                records.append(metrics.QualityRecord(image_id, name, r, err, metrics.psnr(err)))
+    summaries = metrics.summarize(records, psnr_from_avg_mse=config.psnr_from_avg_mse)
+    avg_mse = {(s.transform_name, s.r): s.avg_mse for s in summaries}
+    ape = {}
+    if "dct" in [_name(t) for t in config.transforms]:
+        for s in summaries:
+            ref = avg_mse[("dct", s.r)]
+            ape[(s.transform_name, s.r)] = metrics.ape_vs_dct(s.avg_mse, ref) if ref > 0 else float("nan")
+    return records, summaries, ape
+
+
+def _fmt(x: float) -> str:
+    return format(x, ".6g")  # metrics.format_float (metrics.py:100-102)
+
+
+def write_sweep_outputs(out_dir, config: ExperimentConfig, records, summaries, ape) -> None:
+    """records.csv, summary.csv, run_metadata.json (cli.py:127-152)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    with open(out / "records.csv", "w", newline="") as fp:
+        wr = csv.writer(fp, lineterminator="\n")
+        wr.writerow(["image_id", "transform", "r", "mse", "psnr"])
+        for rec in sorted(records, key=lambda m: (m.transform_name, m.r, m.image_id)):
+            wr.writerow([rec.image_id, rec.transform_name, rec.r, _fmt(rec.mse), _fmt(rec.psnr)])
+    with open(out / "summary.csv", "w") as fp:
+        fp.write("transform,r,compression_ratio,avg_mse,avg_psnr,ape_vs_dct,n_images\n")
+        for s in sorted(summaries, key=lambda m: (m.transform_name, m.r)):
+            cells = [
+                s.transform_name, str(s.r), _fmt(codec.compression_ratio(s.r)), _fmt(s.avg_mse),
+                _fmt(s.avg_psnr), _fmt(ape[(s.transform_name, s.r)]) if ape else "", str(s.n_images),
+            ]
+            fp.write(",".join(cells) + "\n")
+    meta = asdict(config)
+    meta["transforms"] = [_name(t) for t in config.transforms]
+    meta["psnr_convention"] = "psnr_of_avg_mse" if config.psnr_from_avg_mse else "mean_of_per_image_psnr"
+    meta["ape_convention"] = "avg_mse"
+    with open(out / "run_metadata.json", "w") as fp:
+        json.dump(meta, fp, indent=2, sort_keys=True)
+        fp.write("\n")

@@ -132,7 +132,10 @@ def test_entry_points_validate_before_any_cuda_call():
     assert L.adct_compress_retain(n, n, 1, 60, 64, 4096, 4096, 10, n, n, n) == 1  # BadDimensions
     assert L.adct_compress_retain(n, n, -1, 64, 64, 4096, 4096, 10, n, n, n) == 5
     assert L.adct_forward_int32(n, 1, 64, 63, 4096, 0, n, n) == 1
-    assert L.adct_sweep_retain_sse(n, 1, 64, 64, 4096, 5, 4, n, n) == 2
+    assert L.adct_sweep_retain_sse(n, 1, 64, 64, 4096, 5, 4, n, n, n) == 2
+    cm = (ctypes.c_double * 64)()
+    assert L.adct_sweep_dense(n, 0, 1, 64, 64, cm, 0, 5, n, n) == 2
+    assert L.adct_forward_dense(n, 0, 1, 64, 60, cm, n, n) == 1
     assert L.adct_inverse_f64(n, 1, 64, 64, 0, 1, n, n) == 2
     # zero images: nothing to do, no device access
     assert L.adct_compress_retain(n, n, 0, 64, 64, 4096, 4096, 10, n, n, n) == 0

@@ -74,9 +74,13 @@ def test_bad_dimensions_raised_before_compute():
         codec.retain_coefficients(np.zeros((4, 4)), 3)
 
 
-def test_other_transforms_rejected():
-    with pytest.raises(NotImplementedError):
-        codec.compress_image(transforms.exact_dct_matrix(), np.zeros((8, 8)), 3)
+def test_non_8x8_transform_matrix_rejected_before_compute():
+    class Bad:
+        name = "bad"
+        matrix = np.eye(4)
+
+    with pytest.raises(errors.BadDimensions):
+        codec.compress_image(Bad, np.zeros((8, 8)), 3)
 
 
 def test_metrics_host_functions():
