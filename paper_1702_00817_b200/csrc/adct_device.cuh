@@ -326,16 +326,18 @@ struct CtaSum {
   u64 word;  // [63:32] warps arrived, [31:0] partial sum
 };
 
+
 __device__ __forceinline__ void cta_sum_init(CtaSum& s) {
   if (threadIdx.x == 0) s.word = 0;
   __syncthreads();
 }
 
+template <int NT = kThreads>
 __device__ __forceinline__ void cta_sum_add(CtaSum& s, u32 v, u64* dst) {
   v = __reduce_add_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0) {
     const u64 old = atomicAdd(&s.word, (1ull << 32) | (u64)v);
-    if ((u32)(old >> 32) == kThreads / 32 - 1) {
+    if ((u32)(old >> 32) == NT / 32 - 1) {
       const u64 total = (u64)(u32)old + v;
       if (total != 0) atomicAdd(dst, total);
     }
@@ -369,14 +371,15 @@ struct UnitLoc {
   int32_t width;
 };
 
-template <bool PAIR>
+// NT = units per tile = threads per CTA; cta_begin is counted in tiles of NT.
+template <bool PAIR, int NT = kThreads>
 __device__ __forceinline__ bool locate_unit(const PlaneSetDev& ps, UnitLoc& L) {
   const u32 bx = blockIdx.x;
   int p = 0;
   if (ps.n_planes > 1 && bx >= ps.p[1].cta_begin) p = 1;
   if (ps.n_planes > 2 && bx >= ps.p[2].cta_begin) p = 2;
   const PlaneDev& P = ps.p[p];
-  const u32 unit = (bx - P.cta_begin) * kThreads + threadIdx.x;
+  const u32 unit = (bx - P.cta_begin) * NT + threadIdx.x;
   L.plane = p;
   L.frame = (int64_t)ps.frame_base + blockIdx.y;
   L.width = P.width;

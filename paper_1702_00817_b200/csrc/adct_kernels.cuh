@@ -44,13 +44,17 @@ __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
 // ---------------------------------------------------------------------------
 // K2: fused retain-r, r a template parameter (pruned at compile time).
 // ---------------------------------------------------------------------------
+// Retain tiles are 128 units (4 warps): measured faster than 256 for this
+// memory-bound kernel (more, smaller CTAs per SM).
+constexpr int kRetainThreads = 128;
+
 template <int R, bool PAIR>
-__global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __restrict__ sse) {
+__global__ void __launch_bounds__(kRetainThreads) k_retain(PlaneSetDev ps, u64* __restrict__ sse) {
   __shared__ CtaSum cta;
   cta_sum_init(cta);
   UnitLoc L;
   u32 acc = 0;
-  if (locate_unit<PAIR>(ps, L)) {
+  if (locate_unit<PAIR, kRetainThreads>(ps, L)) {
     uint4 w[8];
     load_unit<PAIR>(L.src, L.width, w);
     u32 x[8][8], Z[8][8], W[8][8], U[8][8];
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_retain(PlaneSetDev ps, u64* __rest
     inv2d(W, U);
     acc = emit_unit<PAIR>(U, w, L.dst, L.width);
   }
-  if (sse != nullptr) cta_sum_add(cta, acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr) cta_sum_add<kRetainThreads>(cta, acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // Runtime-r variant: ragged widths (PAIR=false) and the exact "unrounded"

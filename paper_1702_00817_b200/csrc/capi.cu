@@ -43,7 +43,7 @@ struct PlaneSetHost {
 // Validate planes and lay out the tile grid.  `force_single` selects one
 // block per thread (used by k_quant_wide).
 int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, PlaneSetHost& out,
-                 bool force_single = false) {
+                 bool force_single = false, int tile = kThreads) {
   if (planes == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
     return ADCT_ERR_INVALID_ARGUMENT;
   std::memset(&out.dev, 0, sizeof(out.dev));
@@ -92,7 +92,7 @@ int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, Pla
       if ((uint32_t)(((uint64_t)last * m) >> 32) != last / d.upr) return ADCT_ERR_INVALID_ARGUMENT;
     }
     d.cta_begin = cta;
-    cta += (d.units + kThreads - 1) / kThreads;
+    cta += (d.units + tile - 1) / tile;
   }
   for (int k = n_planes; k < 3; ++k) out.dev.p[k].cta_begin = 0xFFFFFFFFu;
   out.dev.n_planes = n_planes;
@@ -396,8 +396,11 @@ static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n
   u64* d_sse = reinterpret_cast<u64*>(sse);
   u64* d_ssef = reinterpret_cast<u64*>(ssef);
   if (ssef == nullptr && ps.pair) {
+    PlaneSetHost ps128;  // the pruned retain kernels run 128-unit tiles
+    rc = build_planes(planes, n_planes, n_frames, ps128, false, kRetainThreads);
+    if (rc != ADCT_OK) return rc;
     RetainKernel k = retain_kernel(r);
-    return for_frame_chunks(ps, n_frames, [&](dim3 g) { k<<<g, kThreads, 0, s>>>(ps.dev, d_sse); });
+    return for_frame_chunks(ps128, n_frames, [&](dim3 g) { k<<<g, kRetainThreads, 0, s>>>(ps128.dev, d_sse); });
   }
   return for_frame_chunks(ps, n_frames, [&](dim3 g) {
     if (ps.pair) {
