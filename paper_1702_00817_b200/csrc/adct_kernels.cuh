@@ -181,7 +181,7 @@ struct TileCursor {
   int32_t width;
 };
 
-template <bool PAIR>
+template <bool PAIR, int NT = kThreads>
 __device__ __forceinline__ TileCursor tile_unit(const PlaneSetDev& ps, int64_t tile, u32 tiles_per_frame) {
   TileCursor c;
   c.frame = tile / tiles_per_frame;
@@ -190,7 +190,7 @@ __device__ __forceinline__ TileCursor tile_unit(const PlaneSetDev& ps, int64_t t
   if (ps.n_planes > 1 && tb >= ps.p[1].cta_begin) p = 1;
   if (ps.n_planes > 2 && tb >= ps.p[2].cta_begin) p = 2;
   const PlaneDev& P = ps.p[p];
-  const u32 unit = (tb - P.cta_begin) * kThreads + threadIdx.x;
+  const u32 unit = (tb - P.cta_begin) * NT + threadIdx.x;
   c.plane = p;
   c.width = P.width;
   c.active = unit < P.units;
@@ -209,12 +209,12 @@ __device__ __forceinline__ TileCursor tile_unit(const PlaneSetDev& ps, int64_t t
   return c;
 }
 
-template <bool PAIR>
+template <bool PAIR, int NT = kThreads>
 __device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor& c) {
   if (!c.active) return;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const u32 sa = (u32)__cvta_generic_to_shared(slot_base + i * kThreads);
+    const u32 sa = (u32)__cvta_generic_to_shared(slot_base + i * NT);
     const uint8_t* g = c.src + (int64_t)i * c.width;
     if (PAIR)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");

@@ -1,6 +1,7 @@
 // capi.cu — extern "C" entry points of libadct_cuda.so (declared in
 // include/adct_cuda.h).  Validation mirrors the reference's contract errors
 // (errors.py:21-33) and happens before anything is enqueued.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
