@@ -138,11 +138,11 @@ int persistent_grid(int* grid) {
   return ADCT_OK;
 }
 
-// ADCT_QUANT_KERNEL=grid selects the one-tile-per-CTA quant kernel (A/B).
-bool use_pipelined_quant() {
-  static const bool v = [] {
+// ADCT_QUANT_KERNEL = pipe (default) | grid selects the quant kernel (A/B).
+int quant_kernel_choice() {
+  static const int v = [] {
     const char* e = std::getenv("ADCT_QUANT_KERNEL");
-    return !(e && std::strcmp(e, "grid") == 0);
+    return (e && std::strcmp(e, "grid") == 0) ? 0 : 1;
   }();
   return v;
 }
@@ -448,7 +448,7 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
   }
   const QParamsDev q = to_qparams(*qtab);
   const bool al = qtab->aligned != 0;
-  if (use_pipelined_quant() && ps.grid_x > 0 && n_frames > 0) {
+  if (quant_kernel_choice() == 1 && ps.grid_x > 0 && n_frames > 0) {
     const int64_t n_tiles = (int64_t)ps.grid_x * n_frames;
     int grid = 0;
     int rc2 = persistent_grid(&grid);
