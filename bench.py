@@ -438,7 +438,7 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-images", type=int, default=256)
-    ap.add_argument("--e2e-chunk-mb", type=int, default=16)
+    ap.add_argument("--e2e-chunk-mb", type=int, default=32)
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
