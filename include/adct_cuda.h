@@ -85,7 +85,7 @@ typedef struct adct_qtab {
   int32_t wide;         /* 1: 16-bit-lane inverse not provably exact -> one block per thread */
   int32_t max_abs_v;    /* proven bound of |64*(x_hat-128)| before clamping */
   int32_t quality;      /* JPEG quality used to build it, or -1 for an explicit table */
-  int32_t aligned;      /* 1: max_abs_v + 32 <= 24576, output window needs no bit flip */
+  int32_t aligned;      /* 1: max_abs_v + 32 <= 24575: fused one-op output clamp, no bit flip */
 } adct_qtab_t;
 
 /* Build from an unrounded Q' table (64 float64, row-major), i.e. the output of

@@ -248,16 +248,17 @@ __device__ __forceinline__ void unpack_unit(const uint4 (&w)[8], u32 (&x)[8][8])
 // pixel = clamp(floor((U - O + 8192) / 64), 0, 255).
 //   FLIP (O = 32768): clamp U to [0x6000, 0x9FFF] (native VIMNMX.U16x2);
 //     (U >> 6) & 0xFF == pixel ^ 0x80, so the packed word is XORed with 0x80.
-//   !FLIP (O = 24576, tables whose proven range allows it): clamp to
-//     [0x4000, 0x7FFF]; (U >> 6) & 0xFF == pixel, no fix-up.
+//   !FLIP (O = 24576, tables with max |64(x_hat-128)| + 32 <= 24575): one
+//     VIADDMNMX.S16x2.RELU computes max(min(U - 16384, 16383), 0) per lane
+//     (the add is lane-wise modulo 2^16 — measured on B200 — and U - 16384
+//     stays inside int16 for these tables), then (F >> 6) == pixel.
 // Shifting by 2 puts bits 6..13 of each lane in bytes 1 and 3 (the bits
 // pushed from lane A into lane B land in byte 2, which is never read), then
 // PRMT gathers the bytes.
 template <bool FLIP>
 __device__ __forceinline__ u32 clamp_shift(u32 U) {
-  constexpr u32 lo = FLIP ? 0x60006000u : 0x40004000u;
-  constexpr u32 hi = FLIP ? 0x9FFF9FFFu : 0x7FFF7FFFu;
-  return __vmaxu2(__vminu2(U, hi), lo) << 2;
+  if (FLIP) return __vmaxu2(__vminu2(U, 0x9FFF9FFFu), 0x60006000u) << 2;
+  return __viaddmin_s16x2_relu(U, 0xC000C000u, 0x3FFF3FFFu) << 2;
 }
 
 template <bool FLIP = true>

@@ -283,7 +283,7 @@ int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out
   if (bound > 1.0e9) return ADCT_ERR_UNSUPPORTED;  // keeps the 32-bit path far from overflow
   out->max_abs_v = (int32_t)std::ceil(bound);
   out->wide = (!packed_ok || bound + 32.0 > 32767.0) ? 1 : 0;
-  out->aligned = (!out->wide && bound + 32.0 <= 24576.0) ? 1 : 0;
+  out->aligned = (!out->wide && bound + 32.0 <= 24575.0) ? 1 : 0;
   out->quality = quality;
   return ADCT_OK;
 }
