@@ -4,7 +4,8 @@ Drop-in for the hot path of the reference package `adct`: the codec and
 metric functions keep their names and signatures (codec.py:24-155,
 metrics.py:24-97) and run on sm_100a kernels in libadct_cuda.so through a C
 ABI (include/adct_cuda.h).  The batched device API lives in `batch`,
-multi-GPU sharding in `shard`, the host-buffer pipeline in `pipeline`.
+multi-GPU sharding in `shard`, the host-buffer pipeline in `pipeline`, the
+GPU-backed corpus sweep in `sweep`, PGM ingestion in `pgm`.
 """
 
 from .codec import (
@@ -27,18 +28,28 @@ from .errors import (
     DuplicateName,
     EmptyGroup,
     InvalidRetention,
+    IoFailure,
+    MalformedHeader,
     NonOrthogonalKernel,
     NonPositiveQuantizer,
+    TruncatedData,
+    UnsupportedMaxval,
     UnsupportedQuantizer,
     ZeroRow,
 )
+from .flowgraph import OpCount, count_operations, fast_forward, flow_intermediates
 from .metrics import CorpusSummary, QualityRecord, ape_vs_dct, mse, psnr, summarize
+from .sweep import ExperimentConfig, run_sweep, write_sweep_outputs
 from .transforms import (
     ApproximateTransform,
     DiagonalScaling,
     ExactDct,
+    KernelRegistry,
     TransformMatrix,
+    derive_scaling,
     exact_dct_matrix,
+    load_registry,
+    parse_kernel_records,
     proposed_kernel,
     proposed_scaling,
     proposed_transform,

@@ -142,3 +142,51 @@ def test_lane_range_bound_for_every_r():
     spec.loader.exec_module(rb)
     worst = max(rb.worst(r) for r in range(1, 65))
     assert worst == 27136 and worst + 32 <= 32767
+
+
+def test_flowgraph_api_kats():
+    from paper_1702_00817_b200 import flowgraph
+
+    y, cost = flowgraph.fast_forward([1, 2, 3, 4, 5, 6, 7, 8])
+    assert y.tolist() == [36, -7, 0, 3, 0, 5, 0, 1] and (cost.additions, cost.multiplications, cost.shifts) == (14, 0, 0)
+    assert flowgraph.fast_forward([1] * 8)[0].tolist() == [8, 0, 0, 0, 0, 0, 0, 0]
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        x = rng.integers(-1024, 1025, 8)
+        assert np.array_equal(flowgraph.fast_forward(x)[0], exact.T @ x)
+    assert max(abs(v) for st in flowgraph.flow_intermediates([255, 0, 255, 0, 0, 255, 0, 255]) for v in st) <= 2040
+
+
+def test_registry_parse_and_scaling(tmp_path):
+    from paper_1702_00817_b200 import errors as E
+    from paper_1702_00817_b200.transforms import derive_scaling, load_registry
+
+    t = exact.T
+    txt = "# test file\nprop\n" + "\n".join(" ".join(str(v) for v in row) for row in t) + "\n14 0 0\n"
+    sgn = np.sign(transforms.exact_dct_matrix().matrix).astype(int)
+    txt += "sdct non-orthogonal\n" + "\n".join(" ".join(str(v) for v in row) for row in sgn) + "\n24 0 0\n"
+    (tmp_path / "k.txt").write_text(txt)
+    reg = load_registry(tmp_path / "k.txt")
+    assert reg.names() == ("prop", "sdct") and len(reg) == 2
+    assert np.allclose(reg.get("prop").scaling.diag, transforms.proposed_scaling().diag)
+    assert reg.get("sdct").orthogonal is False
+    with pytest.raises(E.NonOrthogonalKernel):
+        derive_scaling(sgn)
+    with pytest.raises(E.DuplicateName):
+        reg.register(transforms.TransformMatrix("prop", t))
+
+
+def test_registry_matches_live_reference(reference):
+    """The reference's own data file parses identically here."""
+    import importlib.resources as ir
+
+    from paper_1702_00817_b200.transforms import load_registry
+
+    path = ir.files("adct").joinpath("data/kernels.txt")
+    ours = load_registry(path)
+    ref = reference.default_registry()
+    assert ours.names() == ref.names()
+    for name in ref.names():
+        assert np.array_equal(ours.get(name).kernel.entries, ref.get(name).kernel.entries)
+        assert np.allclose(ours.get(name).scaling.diag, ref.get(name).scaling.diag, rtol=0, atol=1e-15)
+        assert ours.get(name).orthogonal == ref.get(name).orthogonal
