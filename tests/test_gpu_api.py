@@ -191,3 +191,25 @@ def test_many_images_grid_y_chunking(cuda):
     idx = [0, 65534, 65535, 65536, 69999]
     wr, ws, _ = exact.compress_retain(x[idx].cpu().numpy(), 5)
     assert np.array_equal(rec[idx].cpu().numpy(), wr) and np.array_equal(sse[idx].cpu().numpy(), ws)
+
+
+def test_config3_full_batch_properties(cuda):
+    """Full config 3 (4096 x 2048^2, 16 GiB): one launch == 8 chunked launches
+    bit for bit, deterministic across runs, SSE == independent device SSE of
+    (input, reconstruction), and sampled images == the oracle."""
+    nb, smin, smax = synth.CONFIG_BLOBS[3]
+    x = synth.images_device(range(4096), 2048, 2048, nb, smin, smax, device=cuda)
+    rec = torch.empty_like(x)
+    _, sse, _ = batch.compress_retain(x, 10, out=rec)
+    sse_chunks = torch.cat([batch.compress_retain(x[k * 512:(k + 1) * 512], 10, reconstruct=False)[1] for k in range(8)])
+    assert torch.equal(sse, sse_chunks)
+    h1 = torch.sum(rec.view(4096, -1)[:, ::4097].to(torch.int64), dim=1)
+    rec2 = torch.empty_like(x)
+    _, sse2, _ = batch.compress_retain(x, 10, out=rec2)
+    assert torch.equal(sse, sse2) and torch.equal(rec, rec2)
+    del rec2
+    assert torch.equal(batch.sse_u8(x, rec), sse)
+    for i in (0, 1234, 4095):
+        wr, ws, _ = exact.compress_retain(x[i].cpu().numpy(), 10)
+        assert int(sse[i]) == ws and np.array_equal(rec[i].cpu().numpy(), wr)
+    assert int(h1.sum()) > 0
