@@ -731,9 +731,20 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
     std::memset(host_sse, 0, (size_t)n * sizeof(uint64_t));
     return ADCT_OK;
   }
-  const int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
-  if (per < 1) return ADCT_ERR_INVALID_ARGUMENT;  // chunk smaller than one image
   ADCT_CUDA_TRY(cudaSetDevice(p->device));
+  if ((size_t)px > p->chunk_bytes) {  // one image larger than a chunk: grow the staging buffers
+    for (int k = 0; k < adct_pipeline::kDepth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+    const size_t nb = ((size_t)px + 15) / 16 * 16;
+    for (int k = 0; k < adct_pipeline::kDepth; ++k) {
+      ADCT_CUDA_TRY(cudaFree(p->d_in[k]));
+      ADCT_CUDA_TRY(cudaFree(p->d_out[k]));
+      p->d_in[k] = p->d_out[k] = nullptr;
+      ADCT_CUDA_TRY(cudaMalloc(&p->d_in[k], nb));
+      ADCT_CUDA_TRY(cudaMalloc(&p->d_out[k], nb));
+    }
+    p->chunk_bytes = nb;
+  }
+  const int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
   if (n > p->sse_cap) {  // grow the per-call device SSE vector
     if (p->d_sse) ADCT_CUDA_TRY(cudaFree(p->d_sse));
     p->d_sse = nullptr;

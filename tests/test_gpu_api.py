@@ -132,6 +132,9 @@ def test_host_pipeline_retain_and_quant(cuda, chunk_mb):
         assert np.array_equal(rec, wq) and np.array_equal(sseq, wqs)
         _, sse_only = p.compress_retain(imgs, 3)  # SSE only, no reconstruction copy
         assert np.array_equal(sse_only, exact.compress_retain(imgs, 3)[1])
+    with HostPipeline(0, chunk_bytes=4096) as p:  # smaller than one image: staging grows
+        _, sse_small = p.compress_retain(imgs, 10, rec)
+        assert np.array_equal(sse_small, exact.compress_retain(imgs, 10)[1])
 
 
 # --- generator -------------------------------------------------------------------------
