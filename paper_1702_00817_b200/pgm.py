@@ -159,3 +159,31 @@ def compress_files(paths: Sequence[str | os.PathLike], r: int, out_dir: str | os
             Path(out_dir).mkdir(parents=True, exist_ok=True)
             write_pgm_u8(rec[k], Path(out_dir) / (Path(path).stem + f"_r{r}.pgm"))
     return results
+
+
+# --- reference-shaped API (corpus.py:26-121) ------------------------------------
+
+class GrayImage:
+    """8-bit-valued grayscale image with float64 samples (corpus.py:26-43)."""
+
+    def __init__(self, width: int, height: int, samples) -> None:
+        if width <= 0 or height <= 0:
+            raise ValueError("image dimensions must be positive")
+        s = np.array(samples, dtype=np.float64).reshape(height, width)
+        if not np.isfinite(s).all():
+            raise ValueError("samples must be finite")
+        if s.min() < 0 or s.max() > 255:
+            raise ValueError("samples must lie in [0, 255]")
+        s.setflags(write=False)
+        self.width, self.height, self.samples = width, height, s
+
+
+def read_pgm(path) -> GrayImage:
+    """P2/P5 PGM -> GrayImage (corpus.read_pgm contract)."""
+    u8 = read_pgm_u8(path)
+    return GrayImage(u8.shape[1], u8.shape[0], u8)
+
+
+def write_pgm(image: GrayImage, path) -> None:
+    """P5, maxval 255, samples rounded half away from zero (corpus.write_pgm)."""
+    write_pgm_u8(np.floor(np.asarray(image.samples) + 0.5).astype(np.uint8), path)

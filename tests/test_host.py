@@ -190,3 +190,12 @@ def test_registry_matches_live_reference(reference):
         assert np.array_equal(ours.get(name).kernel.entries, ref.get(name).kernel.entries)
         assert np.allclose(ours.get(name).scaling.diag, ref.get(name).scaling.diag, rtol=0, atol=1e-15)
         assert ours.get(name).orthogonal == ref.get(name).orthogonal
+
+
+def test_apply_forward_inverse_kats():
+    t = transforms.proposed_transform()
+    x = np.arange(1, 9, dtype=np.float64)
+    y = transforms.apply_forward(t, x)
+    assert np.allclose(y / t.scaling.diag, [36, -7, 0, 3, 0, 5, 0, 1])
+    assert np.abs(transforms.apply_inverse(t, y) - x).max() < 1e-9
+    assert np.allclose(transforms.apply_inverse(t, np.r_[np.sqrt(8), np.zeros(7)]), np.ones(8))

@@ -70,3 +70,13 @@ def test_compress_files_end_to_end(tmp_path, cuda):
     for k, (name, m, _) in enumerate(res):
         assert name == f"im{k}" and m == ws[k] / (64 * 48)
         assert np.array_equal(pgm.read_pgm_u8(tmp_path / "out" / f"im{k}_r10.pgm"), wr[k])
+
+
+def test_reference_shaped_api(tmp_path):
+    img = pgm.GrayImage(16, 8, np.arange(128, dtype=np.float64).reshape(8, 16) + 0.4)
+    pgm.write_pgm(img, tmp_path / "g.pgm")
+    back = pgm.read_pgm(tmp_path / "g.pgm")
+    assert back.width == 16 and back.height == 8
+    assert np.array_equal(back.samples, np.floor(img.samples + 0.5))
+    with pytest.raises(ValueError):
+        pgm.GrayImage(2, 2, [0, 1, 2, 300])
