@@ -354,9 +354,9 @@ def gpu_arm(args) -> None:
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_src = measured_hbm_peak()
 
-    # ---- end to end: host buffers through the C-ABI pipeline -------------------
+    # ---- end to end: host buffers through the C-ABI pipeline (every rank) -------
     e2e = None
-    if rank == 0 and not args.no_e2e and cfg["kind"] in ("retain", "quant"):
+    if not args.no_e2e and cfg["kind"] in ("retain", "quant"):
         m = min(per, args.e2e_images)
         host_in = imgs[:m].cpu().numpy()
         host_out = np.empty_like(host_in)
@@ -371,13 +371,21 @@ def gpu_arm(args) -> None:
                     call = lambda: pipe.compress_quant(host_in, qt0, host_out, register=False)
                 call()
                 reps = 3
+                if world > 1:
+                    dist.barrier()
                 t0 = time.perf_counter()
                 for _ in range(reps):
-                    _, sse_host = call()
+                    call()
                 dt = (time.perf_counter() - t0) / reps
-            e2e = {"value": m * cfg["h"] * cfg["w"] / dt / 1e9, "unit": UNIT,
-                   "h2d_bytes_per_step": int(host_in.nbytes), "d2h_bytes_per_step": int(host_out.nbytes + 8 * m),
-                   "images_per_step": m, "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline"}
+            if world > 1:
+                t = torch.tensor([dt], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = t.item()
+            e2e = {"value": world * m * cfg["h"] * cfg["w"] / dt / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": int(world * host_in.nbytes),
+                   "d2h_bytes_per_step": int(world * (host_out.nbytes + 8 * m)),
+                   "images_per_step": world * m,
+                   "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks"}
         finally:
             unpin(host_in)
             unpin(host_out)

@@ -697,10 +697,11 @@ int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w, int64_t img_
 struct adct_pipeline {
   int device = 0;
   size_t chunk_bytes = 0;
-  static constexpr int kDepth = 3;
-  cudaStream_t stream[kDepth] = {};
-  uint8_t* d_in[kDepth] = {};
-  uint8_t* d_out[kDepth] = {};
+  static constexpr int kMaxDepth = 8;
+  int depth = 3;  // streams / staging slots in flight (ADCT_PIPELINE_DEPTH, 2..8)
+  cudaStream_t stream[kMaxDepth] = {};
+  uint8_t* d_in[kMaxDepth] = {};
+  uint8_t* d_out[kMaxDepth] = {};
   uint64_t* d_sse = nullptr;  // SSE of a whole call, copied to the host once at the end
   int64_t sse_cap = 0;
 };
@@ -708,7 +709,7 @@ struct adct_pipeline {
 namespace {
 
 void pipeline_free(adct_pipeline* p) {
-  for (int k = 0; k < adct_pipeline::kDepth; ++k) {
+  for (int k = 0; k < p->depth; ++k) {
     if (p->stream[k]) cudaStreamDestroy(p->stream[k]);
     if (p->d_in[k]) cudaFree(p->d_in[k]);
     if (p->d_out[k]) cudaFree(p->d_out[k]);
@@ -733,9 +734,9 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
   }
   ADCT_CUDA_TRY(cudaSetDevice(p->device));
   if ((size_t)px > p->chunk_bytes) {  // one image larger than a chunk: grow the staging buffers
-    for (int k = 0; k < adct_pipeline::kDepth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+    for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
     const size_t nb = ((size_t)px + 15) / 16 * 16;
-    for (int k = 0; k < adct_pipeline::kDepth; ++k) {
+    for (int k = 0; k < p->depth; ++k) {
       ADCT_CUDA_TRY(cudaFree(p->d_in[k]));
       ADCT_CUDA_TRY(cudaFree(p->d_out[k]));
       p->d_in[k] = p->d_out[k] = nullptr;
@@ -757,7 +758,7 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
   // Nothing in the loop blocks the host (no pageable-memory copies).
   int64_t chunk = 0;
   for (int64_t i0 = 0; i0 < n; i0 += per, ++chunk) {
-    const int b = (int)(chunk % adct_pipeline::kDepth);
+    const int b = (int)(chunk % p->depth);
     const int64_t m = (n - i0) < per ? (n - i0) : per;
     cudaStream_t s = p->stream[b];
     ADCT_CUDA_TRY(cudaMemcpyAsync(p->d_in[b], host_img + i0 * px, (size_t)(m * px),
@@ -773,7 +774,7 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
       ADCT_CUDA_TRY(cudaMemcpyAsync(host_rec + i0 * px, p->d_out[b], (size_t)(m * px),
                                     cudaMemcpyDeviceToHost, s));
   }
-  for (int k = 0; k < adct_pipeline::kDepth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+  for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
   ADCT_CUDA_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return ADCT_OK;
 }
@@ -789,8 +790,12 @@ int adct_pipeline_create(int32_t device, size_t chunk_bytes, adct_pipeline_t** o
   if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   p->device = device;
   p->chunk_bytes = (chunk_bytes + 15) / 16 * 16;
+  if (const char* d = std::getenv("ADCT_PIPELINE_DEPTH")) {
+    const int v = std::atoi(d);
+    if (v >= 2 && v <= adct_pipeline::kMaxDepth) p->depth = v;
+  }
   cudaError_t e = cudaSetDevice(device);
-  for (int k = 0; e == cudaSuccess && k < adct_pipeline::kDepth; ++k) {
+  for (int k = 0; e == cudaSuccess && k < p->depth; ++k) {
     e = cudaStreamCreateWithFlags(&p->stream[k], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_in[k], p->chunk_bytes);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_out[k], p->chunk_bytes);

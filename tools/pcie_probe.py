@@ -34,11 +34,14 @@ res["bidir_each"] = 5 * GB / (time.perf_counter() - t) / 1e9
 imgs = torch.randint(0, 256, (256, 2048, 2048), dtype=torch.uint8).numpy()
 out = np.empty_like(imgs)
 pin(imgs); pin(out)
-for mb in (4, 8, 16, 32, 64):
-    with HostPipeline(0, chunk_bytes=mb << 20) as p:
-        p.compress_retain(imgs, 10, out, register=False)
-        t = time.perf_counter()
-        for _ in range(3): p.compress_retain(imgs, 10, out, register=False)
-        res[f"pipeline_chunk{mb}MB_gpix"] = 3 * imgs.size / (time.perf_counter() - t) / 1e9
+import os
+for depth in (2, 3, 4, 6):
+    os.environ["ADCT_PIPELINE_DEPTH"] = str(depth)
+    for mb in (16, 32, 64):
+        with HostPipeline(0, chunk_bytes=mb << 20) as p:
+            p.compress_retain(imgs, 10, out, register=False)
+            t = time.perf_counter()
+            for _ in range(3): p.compress_retain(imgs, 10, out, register=False)
+            res[f"pipeline_d{depth}_chunk{mb}MB_gpix"] = 3 * imgs.size / (time.perf_counter() - t) / 1e9
 unpin(imgs); unpin(out)
 print(json.dumps(res))
