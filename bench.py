@@ -276,10 +276,11 @@ def gpu_arm(args) -> None:
             launches_per_step = 1
         else:
             qtabs = [quant.quant_table(q) for q in cfg["q"]]
-            sses = [torch.empty(per, dtype=torch.int64, device=dev) for _ in qtabs]
+            sse_q = torch.empty((len(qtabs), per), dtype=torch.int64, device=dev)  # one row per quality
+            sse = sse_q.t()  # (per, n_q) view: what the all-reduce exchanges
             def step_kernel():
-                for qt, s in zip(qtabs, sses):
-                    batch.compress_quant(imgs, qt, out=rec, sse_out=s)
+                for k, qt in enumerate(qtabs):
+                    batch.compress_quant(imgs, qt, out=rec, sse_out=sse_q[k])
             launches_per_step = len(qtabs)
             px_rank *= len(qtabs)
     else:  # config 4 planes
@@ -297,7 +298,7 @@ def gpu_arm(args) -> None:
                       torch.cuda.current_stream().cuda_stream)
         launches_per_step = 1
         px_rank = frames * sum(p.shape[1] * p.shape[2] for p in planes)
-        n_total = frames * world
+        n_total = frames * world if args.scaling == "weak" else cfg["frames"]
         per = frames
     torch.cuda.synchronize()
     log(f"[rank {rank}] workload ready in {time.perf_counter() - t_gen:.1f}s: {px_rank / 1e9:.2f} Gpx per step")
