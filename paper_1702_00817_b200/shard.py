@@ -49,6 +49,12 @@ def init_from_env(backend: str | None = None) -> tuple[int, int, int]:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # Test hooks: ADCT_DIST_BACKEND=gloo runs the collectives on the CPU and
+    # ADCT_DEVICE_MAP=0 puts every rank on GPU 0, so the multi-rank logic can
+    # be exercised on a one-GPU box (no kernel ever waits on another rank).
+    if os.environ.get("ADCT_DEVICE_MAP") is not None:
+        local = int(os.environ["ADCT_DEVICE_MAP"])
+    backend = backend or os.environ.get("ADCT_DIST_BACKEND")
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
