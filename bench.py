@@ -40,6 +40,11 @@ CONFIGS = {
             workload="config2: 256 seeded 1024x1024 u8 images per GPU, fused level-shift+fwd+quant(q=10,50,90)+dequant+inv+SSE"),
     4: dict(kind="planes", frames=512, q=75,
             workload="config4: 512 seeded 3840x2160 YCbCr 4:2:0 frames per GPU, fused quant(q=75) of Y+Cb+Cr in one launch"),
+    1: dict(kind="sweep", h=512, w=512, n=45, r=(1, 45), blobs=(16, 8.0, 64.0),
+            workload="config1: 45 seeded 512x512 u8 images, SSE/PSNR for every r=1..45 from one read (k_sweep); "
+                     "11.8 MB, L2-resident and launch bound: value counts image pixels, not pixel-reconstructions"),
+    0: dict(kind="forward", h=512, w=512, n=1, blobs=(16, 8.0, 64.0),
+            workload="config0: 1 seeded 512x512 u8 image, exact int32 T X T^T coefficients (launch bound)"),
 }
 
 
@@ -136,6 +141,24 @@ def _ref_task(args):
     return refport.psnr(m)
 
 
+def _ref_sweep_task(args):
+    """Reference experiment for one image (the paper's Fig. 2 sweep): the
+    coefficients once, then reconstruct + mse + psnr for every r in range."""
+    img, (r0, r1) = args
+    from oracle import refport
+
+    y = refport.coefficient_blocks(img)
+    return [refport.psnr(refport.mse(img, refport.reconstruct_image(y, r, *img.shape))) for r in range(r0, r1 + 1)]
+
+
+def _ref_forward_task(args):
+    """Reference forward: codec.coefficient_blocks of one image (float64)."""
+    img, _ = args
+    from oracle import refport
+
+    return float(refport.coefficient_blocks(img)[0, 0, 0])
+
+
 def cpu_reference_rate(images, r, budget_s: float, cores: int, task=None):
     """Gpixel/s of the reference algorithm over full `images`, one task per
     worker, for about `budget_s` seconds (task: _ref_task or _ref_quant_task)."""
@@ -184,11 +207,14 @@ def reference_arm(args) -> None:
         return
     cfg = CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
-    if cfg["kind"] == "retain":
-        h, w, r = cfg["h"], cfg["w"], cfg["r"]
+    if cfg["kind"] in ("retain", "sweep", "forward"):
+        h, w = cfg["h"], cfg["w"]
         nb, smin, smax = cfg["blobs"]
-        task = _ref_task
-        what = "oracle/refport.py float64 path (codec.compress_image + metrics.mse/psnr)"
+        r, task, what = {
+            "retain": (cfg.get("r"), _ref_task, "oracle/refport.py float64 path (codec.compress_image + metrics.mse/psnr)"),
+            "sweep": (cfg.get("r"), _ref_sweep_task, "oracle/refport.py float64 sweep (coefficients once, reconstruct+mse+psnr per r)"),
+            "forward": (None, _ref_forward_task, "oracle/refport.coefficient_blocks (codec.py:120-131, float64)"),
+        }[cfg["kind"]]
     else:
         from oracle import exact
         from paper_1702_00817_b200.quant import q50_luma
@@ -261,7 +287,31 @@ def gpu_arm(args) -> None:
 
     # ---- workload resident in HBM -------------------------------------------
     t_gen = time.perf_counter()
-    if cfg["kind"] in ("retain", "quant"):
+    if cfg["kind"] in ("sweep", "forward"):
+        per = cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).count
+        first = rank * cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).start
+        nb, smin, smax = cfg["blobs"]
+        imgs = synth.images_device(range(first, first + per), cfg["h"], cfg["w"], nb, smin, smax, device=dev)
+        px_rank = per * cfg["h"] * cfg["w"]
+        n_total = per * world if args.scaling == "weak" else cfg["n"]
+        if cfg["kind"] == "sweep":
+            r0, r1 = cfg["r"]
+            sse = torch.empty((per, r1 - r0 + 1), dtype=torch.int64, device=dev)
+            import ctypes
+            from paper_1702_00817_b200 import _lib
+            def step_kernel():
+                _lib.call("adct_sweep_retain_sse", imgs.data_ptr(), per, cfg["h"], cfg["w"], cfg["h"] * cfg["w"],
+                          r0, r1, sse.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
+        else:
+            coef = torch.empty((per, cfg["h"] * cfg["w"] // 64, 8, 8), dtype=torch.int32, device=dev)
+            sse = torch.zeros((per, 1), dtype=torch.int64, device=dev)
+            import ctypes
+            from paper_1702_00817_b200 import _lib
+            def step_kernel():
+                _lib.call("adct_forward_int32", imgs.data_ptr(), per, cfg["h"], cfg["w"], cfg["h"] * cfg["w"], 0,
+                          coef.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        launches_per_step = 1
+    elif cfg["kind"] in ("retain", "quant"):
         per = cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).count
         first = rank * cfg["n"] if args.scaling == "weak" else shard.shard_range(cfg["n"], rank, world).start
         nb, smin, smax = cfg["blobs"]
@@ -351,7 +401,8 @@ def gpu_arm(args) -> None:
     total_px = px_rank * world * args.steps
     value = total_px / (elapsed_ms * 1e-3) / 1e9
     px_launch = px_rank / launches_per_step
-    alg_bytes = 2 * px_launch + 8 * per  # u8 in + u8 out (+ 8 B SSE per image)
+    bytes_per_px = {"sweep": 1, "forward": 5}.get(cfg["kind"], 2)  # u8 in (+ u8 out | + int32 coefficients)
+    alg_bytes = bytes_per_px * px_launch + 8 * per * (sse.shape[1] if sse.dim() > 1 else 1)
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_src = measured_hbm_peak()
 
@@ -395,10 +446,11 @@ def gpu_arm(args) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
-        if cfg["kind"] == "retain":
+        if cfg["kind"] in ("retain", "sweep", "forward"):
             sample_imgs = [imgs[k].cpu().numpy() for k in range(min(per, 8))]
-            v, info = cpu_reference_rate(sample_imgs, cfg["r"], args.cpu_seconds, cores)
-            algo = "oracle/refport.py = reference codec.compress_image + metrics.mse/psnr float64 algorithm"
+            task = {"retain": _ref_task, "sweep": _ref_sweep_task, "forward": _ref_forward_task}[cfg["kind"]]
+            v, info = cpu_reference_rate(sample_imgs, cfg.get("r"), args.cpu_seconds, cores, task=task)
+            algo = f"oracle/refport.py = reference float64 algorithm ({task.__doc__.split(chr(10))[0] if task.__doc__ else 'codec.compress_image + metrics.mse/psnr'})"
         else:
             from oracle import exact
 
@@ -420,7 +472,8 @@ def gpu_arm(args) -> None:
             "data": "synthetic (seeded Gaussian blobs + N(0,4^2) noise, BASELINE.json generator, rendered on GPU)",
             "config": {"workload": cfg["workload"], "units_per_gpu": per, "pixels_per_step": px_rank * world,
                        "parallelism": f"dp{world} (images sharded, SSE all-reduce)",
-                       "l2": "inputs >> 126 MB L2 (no flush needed)"},
+                       "l2": "inputs >> 126 MB L2 (no flush needed)" if px_rank > (256 << 20)
+                             else "inputs L2-resident (launch/ALU bound config; no roofline claim)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
@@ -440,7 +493,8 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS),
+                    help="3 (default, large-batch headline), 4, 2, 1 (sweep), 0 (forward)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
