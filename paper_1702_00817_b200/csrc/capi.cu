@@ -151,10 +151,10 @@ QParamsDev to_qparams(const adct_qtab_t& t) {
   QParamsDev q;
   const uint32_t dc_out = t.aligned ? 24576u : 32768u;  // output-field offset (see pack_row)
   for (int p = 0; p < 64; ++p) {
-    q.magic[p] = t.magic[p];
-    q.mult[p] = (uint32_t)t.mult[p];
-    q.bm[p] = (uint32_t)t.bias[p] * (uint32_t)t.mult[p] * 65537u;
-    q.qe[p] = (uint32_t)t.qe[p];
+    q.pos[p].x = t.magic[p];
+    q.pos[p].y = (uint32_t)t.mult[p];
+    q.pos[p].z = (uint32_t)t.bias[p] * (uint32_t)t.mult[p] * 65537u;
+    q.pos[p].w = (uint32_t)t.qe[p];
     q.wadd[p] = (uint32_t)0 - (uint32_t)t.kq[p] * (uint32_t)t.qe[p] * 65537u;
   }
   q.wadd[0] += (dc_out + 32u) * 65537u;
