@@ -51,11 +51,20 @@ def _img_stride(images: torch.Tensor) -> int:
     return images.stride(0) if n > 1 else h * w
 
 
-def forward_int(images: torch.Tensor, *, level_shift: bool = False, dtype=torch.int32) -> torch.Tensor:
-    """K1: T X T^T of every 8x8 block, (N, H*W/64, 8, 8) in `_tile` order (codec.py:74-81, 107-109)."""
+def forward_int(images: torch.Tensor, *, level_shift: bool = False, dtype=torch.int32,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1: T X T^T of every 8x8 block, (N, H*W/64, 8, 8) in `_tile` order (codec.py:74-81, 107-109).
+    `out` (contiguous, int32 or int16, that shape) is written in place when given."""
     images = _as_batch(images)
     n, h, w = images.shape
-    out = torch.empty((n, (h // 8) * (w // 8), 8, 8), dtype=dtype, device=images.device)
+    shape = (n, (h // 8) * (w // 8), 8, 8)
+    if out is None:
+        out = torch.empty(shape, dtype=dtype, device=images.device)
+    elif tuple(out.shape) != shape or not out.is_contiguous() or out.device != images.device:
+        raise ValueError(f"out must be a contiguous {shape} tensor on {images.device}")
+    dtype = out.dtype
+    if dtype not in (torch.int32, torch.int16):
+        raise ValueError("coefficients are int32 or int16")
     name = {torch.int32: "adct_forward_int32", torch.int16: "adct_forward_int16"}[dtype]
     _lib.call(name, _ptr(images), n, h, w, _img_stride(images), int(level_shift), _ptr(out), _stream())
     return out

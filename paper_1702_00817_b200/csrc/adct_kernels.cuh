@@ -376,65 +376,83 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------------------
 // K1: forward integer transform, coefficients in _tile order.
+// The output block of unit u is 2u (pair) or u, so a warp's output is one
+// contiguous run of 32 units x 2 blocks.  Each thread writes one block at a
+// time into a swizzled per-warp shared-memory stage (row = lane, 16-byte
+// piece k at k ^ lane, conflict-free both ways) and the warp then stores it
+// as whole 256/128-byte block runs: 512 contiguous bytes per store
+// instruction instead of 16-byte pieces at a 512-byte stride.
 // ---------------------------------------------------------------------------
+constexpr int kForwardThreads = 128;
+
 template <bool PAIR, typename OutT>
-__global__ void __launch_bounds__(kThreads)
-    k_forward(PlaneSetDev ps, int level_shift, int32_t nbc, OutT* __restrict__ coef) {
+__global__ void __launch_bounds__(kForwardThreads)
+    k_forward(PlaneSetDev ps, int level_shift, OutT* __restrict__ coef) {
+  constexpr int S = 64 * (int)sizeof(OutT);  // bytes per block
+  constexpr int NP = S / 16;                 // 16-byte pieces per block (16 or 8)
+  constexpr int OB = (PAIR ? 2 : 1) * S;     // bytes per unit
+  __shared__ uint4 stage[kForwardThreads / 32][32 * NP];
   const PlaneDev& P = ps.p[0];
-  const u32 unit = blockIdx.x * kThreads + threadIdx.x;
-  if (unit >= P.units) return;
+  const int lane = threadIdx.x & 31;
+  const u32 unit0 = blockIdx.x * kForwardThreads + (threadIdx.x & ~31u);
+  const u32 unit = unit0 + lane;
+  const bool active = unit < P.units;
   const int64_t frame = (int64_t)ps.frame_base + blockIdx.y;
-  const u32 brow = unit / P.upr;
-  const u32 ucol = unit - brow * P.upr;
-  const uint8_t* src =
-      P.src + frame * P.src_fs + (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
-  uint4 w[8];
-  load_unit<PAIR>(src, P.width, w);
-  u32 x[8][8], Z[8][8];
-  unpack_unit(w, x);
-  fwd2d(x, Z);
-  const int64_t nblocks = (int64_t)nbc * (P.units / P.upr);
-  const int64_t blk = frame * nblocks + (int64_t)brow * nbc + (int64_t)ucol * (PAIR ? 2 : 1);
-  OutT* ca = coef + blk * 64;
-  OutT* cb = ca + 64;
+  u32 Z[8][8];
+  if (active) {
+    const u32 brow = unit / P.upr;
+    const u32 ucol = unit - brow * P.upr;
+    const uint8_t* src =
+        P.src + frame * P.src_fs + (int64_t)brow * 8 * P.width + (int64_t)ucol * (PAIR ? 16 : 8);
+    uint4 w[8];
+    load_unit<PAIR>(src, P.width, w);
+    u32 x[8][8];
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+  }
   const u32 dc_shift = level_shift ? 8192u * 65537u : 0u;
-  if (sizeof(OutT) == 4) {
+  // level shift at DC, then bias both lanes to unsigned fields
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int4 va, vb;
-        int* pa = &va.x;
-        int* pb = &vb.x;
+    for (int v = 0; v < 8; ++v) Z[u][v] += 0x8000u - ((u == 0 && v == 0) ? dc_shift : 0u);
+  uint4* st = stage[threadIdx.x >> 5];
+  uint8_t* base = reinterpret_cast<uint8_t*>(coef) + (frame * (int64_t)P.units + unit0) * OB;
+  const int n_here = (int)min(32u, P.units > unit0 ? P.units - unit0 : 0u);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int v = h * 4 + k;
-          const u32 z = Z[u][v] + 0x8000u - ((u == 0 && v == 0) ? dc_shift : 0u);
-          pa[k] = (int)(z & 0xFFFFu) - 32768;
-          pb[k] = (int)z >> 16;
+  for (int half = 0; half < (PAIR ? 2 : 1); ++half) {
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        uint4 piece;
+        if (sizeof(OutT) == 4) {  // piece k = coefficients [4k, 4k+4) of the block
+          const int u = k >> 1, v0 = (k & 1) * 4;
+          u32* e = &piece.x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const u32 z = Z[u][v0 + j];
+            e[j] = half == 0 ? (u32)((int)(z & 0xFFFFu) - 32768) : (u32)((int)z >> 16);
+          }
+        } else {  // piece k = row k of the block, 8 int16
+          const int u = k;
+          u32* e = &piece.x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const u32 z0 = Z[u][2 * j], z1 = Z[u][2 * j + 1];
+            e[j] = half == 0 ? (__byte_perm(z0, z1, 0x5410) ^ 0x80008000u) : __byte_perm(z0, z1, 0x7632);
+          }
         }
-        reinterpret_cast<int4*>(ca)[u * 2 + h] = va;
-        if (PAIR) reinterpret_cast<int4*>(cb)[u * 2 + h] = vb;
+        st[lane * NP + (k ^ (lane & (NP - 1)))] = piece;
       }
-  } else {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      u32 za[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v)
-        za[v] = Z[u][v] + 0x8000u - ((u == 0 && v == 0) ? dc_shift : 0u);
-      uint4 va, vb;
-      va.x = __byte_perm(za[0], za[1], 0x5410) ^ 0x80008000u;
-      va.y = __byte_perm(za[2], za[3], 0x5410) ^ 0x80008000u;
-      va.z = __byte_perm(za[4], za[5], 0x5410) ^ 0x80008000u;
-      va.w = __byte_perm(za[6], za[7], 0x5410) ^ 0x80008000u;
-      vb.x = __byte_perm(za[0], za[1], 0x7632);
-      vb.y = __byte_perm(za[2], za[3], 0x7632);
-      vb.z = __byte_perm(za[4], za[5], 0x7632);
-      vb.w = __byte_perm(za[6], za[7], 0x7632);
-      reinterpret_cast<uint4*>(ca)[u] = va;
-      if (PAIR) reinterpret_cast<uint4*>(cb)[u] = vb;
     }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const int g = j * 32 + lane;  // piece g of the warp's run: thread t = g / NP, piece k
+      const int t = g / NP, k = g % NP;
+      if (t < n_here) st_stream16(base + (int64_t)t * OB + half * S + k * 16, st[t * NP + (k ^ (t & (NP - 1)))]);
+    }
+    __syncwarp();
   }
 }
 

@@ -351,24 +351,24 @@ static int forward_common(const uint8_t* img, int64_t n, int32_t h, int32_t w, i
   if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
   adct_plane_t pl = single_plane(img, nullptr, h, w, img_stride, 0);
   PlaneSetHost ps;
-  int rc = build_planes(&pl, 1, n, ps);
+  int rc = build_planes(&pl, 1, n, ps, false, kForwardThreads);
   if (rc != ADCT_OK) return rc;
   if (ps.grid_x == 0 || n == 0) return ADCT_OK;
   if (coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   if (!aligned(coef, 16)) return ADCT_ERR_MISALIGNED;
-  const int32_t nbc = w / 8;
   cudaStream_t s = as_stream(stream);
+  const int T = kForwardThreads;
   return for_frame_chunks(ps, n, [&](dim3 g) {
     if (out16) {
       if (ps.pair)
-        k_forward<true, int16_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int16_t*)coef);
+        k_forward<true, int16_t><<<g, T, 0, s>>>(ps.dev, level_shift, (int16_t*)coef);
       else
-        k_forward<false, int16_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int16_t*)coef);
+        k_forward<false, int16_t><<<g, T, 0, s>>>(ps.dev, level_shift, (int16_t*)coef);
     } else {
       if (ps.pair)
-        k_forward<true, int32_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int32_t*)coef);
+        k_forward<true, int32_t><<<g, T, 0, s>>>(ps.dev, level_shift, (int32_t*)coef);
       else
-        k_forward<false, int32_t><<<g, kThreads, 0, s>>>(ps.dev, level_shift, nbc, (int32_t*)coef);
+        k_forward<false, int32_t><<<g, T, 0, s>>>(ps.dev, level_shift, (int32_t*)coef);
     }
   });
 }

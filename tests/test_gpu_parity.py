@@ -36,6 +36,23 @@ def test_forward_int_shapes(cuda, shape, level_shift):
         assert np.array_equal(z.cpu().numpy().astype(np.int64), want)
 
 
+@pytest.mark.parametrize("shape", [(5, 136, 272), (3, 72, 200), (70, 24, 48), (2, 8, 4096)])
+def test_forward_int_ragged_warp_runs(cuda, shape):
+    """Units per frame not a multiple of the 32-unit warp run (pair and
+    single-block layouts), many frames, and a frame-strided batch."""
+    n, h, w = shape
+    g = torch.Generator(device="cpu").manual_seed(n * h + w)
+    big = torch.randint(0, 256, (n, h * w + 48), dtype=torch.uint8, generator=g).to(cuda)
+    x = big.as_strided((n, h, w), (h * w + 48, w, 1))
+    want = exact.forward_unscaled(x.cpu().numpy(), level_shift=True)
+    for dt in (torch.int32, torch.int16):
+        out = torch.full((n, h * w // 64, 8, 8), 7, dtype=dt, device=cuda)
+        z = batch.forward_int(x, level_shift=True, out=out)
+        torch.cuda.synchronize()
+        assert z.data_ptr() == out.data_ptr()
+        assert np.array_equal(z.cpu().numpy().astype(np.int64), want)
+
+
 @pytest.mark.parametrize("r", [1, 2, 3, 6, 10, 15, 25, 36, 45, 55, 63, 64])
 def test_retain_matches_oracle(cuda, r):
     x = _imgs(cuda, [3, 4])
