@@ -364,6 +364,18 @@ def gpu_arm(args) -> None:
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    graphed = False
+    if cfg["kind"] in ("sweep", "forward") and not args.no_graph:
+        # launch-bound configs (one small launch per step): replay the step's
+        # C-ABI launch from a CUDA graph so host-side call overhead does not
+        # leave the GPU idle between steps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_kernel()
+        graph.replay()
+        torch.cuda.synchronize()
+        step_kernel = graph.replay
+        graphed = True
 
     # ---- timed region ----------------------------------------------------------
     stream = torch.cuda.current_stream()
@@ -480,6 +492,7 @@ def gpu_arm(args) -> None:
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
+            "cuda_graph": graphed,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -498,6 +511,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="configs 0/1: launch through the C ABI every step")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-images", type=int, default=256)
