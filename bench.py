@@ -276,7 +276,7 @@ def gpu_arm(args) -> None:
     import torch.distributed as dist
 
     from paper_1702_00817_b200 import batch, quant, shard, synth
-    from paper_1702_00817_b200.pipeline import HostPipeline, pin, unpin
+    from paper_1702_00817_b200.pipeline import HostPipeline, pinned_empty
 
     rank, world, local = shard.init_from_env()
     torch.cuda.set_device(local)
@@ -422,10 +422,11 @@ def gpu_arm(args) -> None:
     e2e = None
     if not args.no_e2e and cfg["kind"] in ("retain", "quant"):
         m = min(per, args.e2e_images)
-        host_in = imgs[:m].cpu().numpy()
-        host_out = np.empty_like(host_in)
-        pin(host_in)
-        pin(host_out)
+        # page-locked host buffers from adct_host_alloc (cudaHostAlloc); the
+        # input batch is filled from the device copy before the timed region
+        host_in = pinned_empty(tuple(imgs[:m].shape))
+        host_out = pinned_empty(host_in.shape)
+        host_in[...] = imgs[:m].cpu().numpy()
         try:
             with HostPipeline(local, chunk_bytes=args.e2e_chunk_mb << 20) as pipe:
                 if cfg["kind"] == "retain":
@@ -451,8 +452,7 @@ def gpu_arm(args) -> None:
                    "images_per_step": world * m,
                    "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks"}
         finally:
-            unpin(host_in)
-            unpin(host_out)
+            del host_in, host_out
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None

@@ -223,7 +223,9 @@ int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w,
  * Host-buffer pipeline (the end-to-end entry point).  Streams batches of
  * host images through the device in chunks: H2D copy of chunk i+1, fused
  * compress of chunk i and D2H copy of chunk i-1 overlap on separate streams.
- * Host buffers should be pinned (adct_host_register) for full speed.
+ * Host buffers should be pinned for full speed: adct_host_alloc memory
+ * (cudaHostAlloc) reaches the PCIe limit; adct_host_register'd memory runs
+ * ~9 % slower on the B200 boxes measured (tools/pcie_probe2.py).
  * ------------------------------------------------------------------------- */
 typedef struct adct_pipeline adct_pipeline_t;
 
@@ -239,6 +241,9 @@ int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img,
 /* Page-lock / unlock caller memory (cudaHostRegister). */
 int adct_host_register(void* ptr, size_t bytes);
 int adct_host_unregister(void* ptr);
+/* Page-locked host allocation (cudaHostAlloc, portable); *out = NULL for 0 bytes. */
+int adct_host_alloc(size_t bytes, void** out);
+int adct_host_free(void* ptr);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,8 @@ PROTOTYPES = {
     ),
     "adct_host_register": (c_int, [c_void_p, c_size_t]),
     "adct_host_unregister": (c_int, [c_void_p]),
+    "adct_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),
+    "adct_host_free": (c_int, [c_void_p]),
 }
 
 # C error codes -> exception classes mirroring adct/errors.py:21-33.

@@ -838,4 +838,18 @@ int adct_host_unregister(void* ptr) {
   return ADCT_OK;
 }
 
+int adct_host_alloc(size_t bytes, void** out) {
+  if (out == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (bytes == 0) return ADCT_OK;
+  ADCT_CUDA_TRY(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  return ADCT_OK;
+}
+
+int adct_host_free(void* ptr) {
+  if (ptr == nullptr) return ADCT_OK;
+  ADCT_CUDA_TRY(cudaFreeHost(ptr));
+  return ADCT_OK;
+}
+
 }  // extern "C"

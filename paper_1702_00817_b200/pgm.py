@@ -102,19 +102,21 @@ def read_pgm_u8(path: str | os.PathLike, out: np.ndarray | None = None) -> np.nd
 
 
 def load_batch(paths: Sequence[str | os.PathLike], *, pinned: bool = True) -> np.ndarray:
-    """All files (same size) into one (N, H, W) uint8 buffer, page-locked for
-    the host pipeline when `pinned` (release with pipeline.unpin)."""
+    """All files (same size) into one (N, H, W) uint8 buffer; when `pinned`,
+    the buffer is page-locked host memory (pipeline.pinned_empty, freed with
+    the array) that the host pipeline streams at the PCIe limit."""
     if not paths:
         raise ValueError("no files")
     with open(paths[0], "rb") as f:
         _, w, h, _, _ = parse_header(f.read(4096))
-    batch = np.empty((len(paths), h, w), dtype=np.uint8)
+    if pinned:
+        from .pipeline import pinned_empty
+
+        batch = pinned_empty((len(paths), h, w))
+    else:
+        batch = np.empty((len(paths), h, w), dtype=np.uint8)
     for k, p in enumerate(paths):
         read_pgm_u8(p, batch[k])
-    if pinned:
-        from .pipeline import pin
-
-        pin(batch)
     return batch
 
 
@@ -137,19 +139,12 @@ def compress_files(paths: Sequence[str | os.PathLike], r: int, out_dir: str | os
     """End to end: PGM files -> pinned batch -> GPU retain-r -> per-file (mse, psnr)
     of the rounded reconstruction; optionally writes the reconstructions."""
     from .metrics import psnr
-    from .pipeline import HostPipeline, unpin
+    from .pipeline import HostPipeline, pinned_empty
 
     imgs = load_batch(paths, pinned=True)
-    rec = np.empty_like(imgs)
-    from .pipeline import pin
-
-    pin(rec)
-    try:
-        with HostPipeline(device, chunk_bytes=chunk_bytes) as p:
-            _, sse = p.compress_retain(imgs, r, rec, register=False)
-    finally:
-        unpin(imgs)
-        unpin(rec)
+    rec = pinned_empty(imgs.shape)
+    with HostPipeline(device, chunk_bytes=chunk_bytes) as p:
+        _, sse = p.compress_retain(imgs, r, rec, register=False)
     n_px = imgs.shape[1] * imgs.shape[2]
     results = []
     for k, path in enumerate(paths):

@@ -91,6 +91,26 @@ class _Pinned:
         self.done = []
 
 
+def pinned_empty(shape, dtype=np.uint8) -> np.ndarray:
+    """Uninitialised numpy array in page-locked memory from adct_host_alloc
+    (cudaHostAlloc): the fastest host buffer for the pipeline.  The memory is
+    freed when the array (and every view of it) is garbage collected; do not
+    pin()/unpin() it."""
+    import weakref
+
+    dtype = np.dtype(dtype)
+    shape = tuple(int(d) for d in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
+    if nbytes == 0:
+        return np.empty(shape, dtype)
+    ptr = ctypes.c_void_p()
+    _lib.call("adct_host_alloc", nbytes, ctypes.byref(ptr))
+    buf = (ctypes.c_uint8 * nbytes).from_address(ptr.value)
+    arr = np.frombuffer(buf, dtype=dtype).reshape(shape)
+    weakref.finalize(buf, _lib.lib().adct_host_free, ptr.value)
+    return arr
+
+
 def pin(array: np.ndarray) -> None:
     """Page-lock an array for repeated pipeline calls (unpin() to release)."""
     _lib.call("adct_host_register", array.ctypes.data, array.nbytes)

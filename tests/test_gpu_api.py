@@ -137,6 +137,30 @@ def test_host_pipeline_retain_and_quant(cuda, chunk_mb):
         assert np.array_equal(sse_small, exact.compress_retain(imgs, 10)[1])
 
 
+def test_pinned_empty_buffers_through_pipeline(cuda):
+    import gc
+
+    from paper_1702_00817_b200.pipeline import pinned_empty
+
+    imgs = synth.images_np(range(30, 35), 128, 192, 16, 8.0, 64.0)
+    host_in = pinned_empty(imgs.shape)
+    host_out = pinned_empty(imgs.shape)
+    assert host_in.shape == imgs.shape and host_in.dtype == np.uint8 and host_in.flags.c_contiguous
+    host_in[...] = imgs
+    with HostPipeline(0, chunk_bytes=1 << 16) as p:
+        _, sse = p.compress_retain(host_in, 10, host_out, register=False)
+    wr, ws, _ = exact.compress_retain(imgs, 10)
+    assert np.array_equal(host_out, wr) and np.array_equal(sse, ws)
+    view = host_out[1:3]  # a view keeps the allocation alive
+    del host_out
+    gc.collect()
+    assert np.array_equal(view, wr[1:3])
+    assert pinned_empty((0, 8, 8)).size == 0
+    f = pinned_empty(16, dtype=np.float64)
+    f[:] = 1.5
+    assert f.sum() == 24.0
+
+
 # --- generator -------------------------------------------------------------------------
 
 def test_device_generator_matches_numpy_mirror(cuda):
