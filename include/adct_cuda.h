@@ -77,7 +77,8 @@ typedef struct adct_qtab {
   int32_t mult[64];
   int32_t kq[64];
   /* Scalar quantiser (any table): U = 2Z - [Z<0] + cadd,
-   *   q = (umulhi(U, magic_w) >> shift_w) - kw. */
+   *   q = umulhi(U, magic_w) - kw  (divisor 2Q'; shift_w is always 0 and is
+   *   kept for layout: for Q' > 16384 the quotient window is identically 0). */
   uint32_t magic_w[64];
   int32_t cadd_w[64];
   int32_t kw[64];

@@ -22,11 +22,7 @@ struct QParamsDev {
 };
 
 struct QParamsWide {  // scalar quantiser of k_quant_wide
-  u32 magic[64];
-  u32 cadd[64];
-  int32_t kbias[64];
-  int32_t shift[64];
-  int32_t qe[64];
+  uint4 pos[64];  // x: magic, y: cadd, z: qe, w: wadd = -kw*qe (+ 32 + 8192 at DC)
 };
 
 // Quantise + dequantise one coefficient position of both blocks, returning
@@ -484,10 +480,11 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int p = u * 8 + v;
+        const uint4 k = q.pos[p];
         const int z = Zc[u] - (p == 0 ? 8192 : 0);  // level shift
-        const u32 U = (u32)(2 * z + (z >> 31)) + q.cadd[p];
-        const int qq = (int)(__umulhi(U, q.magic[p]) >> q.shift[p]) - q.kbias[p];
-        Wc[u] = qq * q.qe[p] + (p == 0 ? 32 + 8192 : 0);  // rounding, +128 back
+        const u32 U = (u32)(2 * z + (z >> 31)) + k.y;
+        const u32 h = __umulhi(U, k.x);  // q + kw
+        Wc[u] = (int)h * (int)k.z + (int)k.w;  // (h - kw) * qe (+ rounding, +128 back at DC)
       }
       inv8(Wc, cc);
 #pragma unroll
@@ -497,11 +494,14 @@ __global__ void __launch_bounds__(kThreads)
     for (int i = 0; i < 8; ++i) inv8(c[i], V[i]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      u32 px[8];
+      // |V >> 6| < 2^15: clamp two pixels per packed 16x2 min/relu
+      u32 h2[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) px[j] = (u32)min(max(V[i][j] >> 6, 0), 255);
-      const u32 lo = __byte_perm(__byte_perm(px[0], px[1], 0x0040), __byte_perm(px[2], px[3], 0x0040), 0x5410);
-      const u32 hi = __byte_perm(__byte_perm(px[4], px[5], 0x0040), __byte_perm(px[6], px[7], 0x0040), 0x5410);
+      for (int j = 0; j < 4; ++j)
+        h2[j] = __vimin_s16x2_relu(__byte_perm((u32)(V[i][2 * j] >> 6), (u32)(V[i][2 * j + 1] >> 6), 0x5410),
+                                   0x00FF00FFu);
+      const u32 lo = __byte_perm(h2[0], h2[1], 0x6420);
+      const u32 hi = __byte_perm(h2[2], h2[3], 0x6420);
       if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width, make_uint2(lo, hi));
       acc = sse4(w[i].x, lo, acc);
       acc = sse4(w[i].y, hi, acc);

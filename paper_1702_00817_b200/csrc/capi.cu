@@ -164,12 +164,12 @@ QParamsDev to_qparams(const adct_qtab_t& t) {
 QParamsWide to_qparams_wide(const adct_qtab_t& t) {
   QParamsWide q;
   for (int p = 0; p < 64; ++p) {
-    q.magic[p] = t.magic_w[p];
-    q.cadd[p] = (uint32_t)t.cadd_w[p];
-    q.kbias[p] = t.kw[p];
-    q.shift[p] = t.shift_w[p];
-    q.qe[p] = t.qe[p];
+    q.pos[p].x = t.magic_w[p];
+    q.pos[p].y = (uint32_t)t.cadd_w[p];
+    q.pos[p].z = (uint32_t)t.qe[p];
+    q.pos[p].w = (uint32_t)0 - (uint32_t)t.kw[p] * (uint32_t)t.qe[p];
   }
+  q.pos[0].w += 32u + 8192u;  // rounding, +128 back (64 * 128)
   return q;
 }
 
@@ -247,24 +247,20 @@ int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out
       if (K < 0) K = 0;
       const int64_t C = Q * (2 * K + 1);
       if (C + 2 * kZmax >= (1ll << 32)) return ADCT_ERR_UNSUPPORTED;
-      int found = -1;
-      uint64_t mw = 0;
-      for (int sh = 0; sh < 16 && found < 0; ++sh) {
-        const uint64_t m = ((1ull << (32 + sh)) + (uint64_t)D - 1) / (uint64_t)D;
-        if (m > 0xFFFFFFFFull) break;
-        bool ok = true;
-        for (int64_t Z = -kZmax; Z <= kZmax; ++Z) {
-          const int64_t U = 2 * Z - (Z < 0 ? 1 : 0) + C;
-          const int64_t got = (int64_t)((((uint64_t)U * m) >> 32) >> sh) - K;
-          if (U < 0 || got != rha_div(Z, Q)) { ok = false; break; }
-        }
-        if (ok) { found = sh; mw = m; }
+      // umulhi alone is exact over the reachable window (for Q' > 16384 the
+      // quotient is identically 0); shift_w stays 0 (field kept for layout).
+      const uint64_t mw = ((1ull << 32) + (uint64_t)D - 1) / (uint64_t)D;
+      bool ok = mw <= 0xFFFFFFFFull;
+      for (int64_t Z = -kZmax; ok && Z <= kZmax; ++Z) {
+        const int64_t U = 2 * Z - (Z < 0 ? 1 : 0) + C;
+        const int64_t got = (int64_t)(((uint64_t)U * mw) >> 32) - K;
+        if (U < 0 || got != rha_div(Z, Q)) ok = false;
       }
-      if (found < 0) return ADCT_ERR_UNSUPPORTED;
+      if (!ok) return ADCT_ERR_UNSUPPORTED;
       out->magic_w[p] = (uint32_t)mw;
       out->cadd_w[p] = (int32_t)C;
       out->kw[p] = (int32_t)K;
-      out->shift_w[p] = found;
+      out->shift_w[p] = 0;
     }
   }
   // |64 (x_hat - 128)| <= 8192 + max_ij sum_uv |T_ui T_vj| E_uv Q'_uv / 2

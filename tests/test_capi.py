@@ -102,6 +102,34 @@ def test_qtab_quantiser_constants_are_exact():
         assert np.array_equal(got, want), q
 
 
+def test_qtab_scalar_quantiser_constants_are_exact():
+    """The wide (one block per thread) quantiser's constants over the whole
+    supported Q' range (1 .. 2^20): multiply-high alone, no post-shift."""
+    rng = np.random.default_rng(3)
+    tables = [quant.quant_table(q) for q in (1, 10, 24)]
+    tables.append(quant.quant_table(qprime_unrounded=rng.choice(
+        [1.0, 3.0, 40000.0, 65536.0, 300001.0, 1048576.0], size=(8, 8))))
+    # Q' across the whole supported range, incl. near powers of two
+    grid = np.unique(np.concatenate([np.geomspace(1, 2**20, 40).round(), 2.0 ** np.arange(21),
+                                     2.0 ** np.arange(1, 21) - 1, 2.0 ** np.arange(1, 21) + 1]))
+    grid = grid[grid <= 2**20]
+    for k in range(0, len(grid), 64):
+        chunk = np.resize(grid[k:k + 64], 64)
+        tables.append(quant.quant_table(qprime_unrounded=chunk.reshape(8, 8)))
+    Z = np.arange(-8192, 8193, dtype=np.int64)
+    for t in tables:
+        Qp = quant.qtab_qprime(t).reshape(64)
+        want = np.sign(Z)[None, :] * ((2 * np.abs(Z)[None, :] + Qp[:, None]) // (2 * Qp[:, None]))
+        mag = np.frombuffer(bytes(t.magic_w), dtype=np.uint32).astype(np.uint64)
+        cadd = np.frombuffer(bytes(t.cadd_w), dtype=np.int32).astype(np.int64)
+        kw = np.frombuffer(bytes(t.kw), dtype=np.int32).astype(np.int64)
+        assert not np.frombuffer(bytes(t.shift_w), dtype=np.int32).any()
+        U = (2 * Z - (Z < 0))[None, :] + cadd[:, None]
+        assert U.min() >= 0 and U.max() < 2**32
+        got = ((U.astype(np.uint64) * mag[:, None]) >> np.uint64(32)).astype(np.int64) - kw[:, None]
+        assert np.array_equal(got, want)
+
+
 def test_qtab_build_from_fold_and_errors():
     from paper_1702_00817_b200 import transforms
 

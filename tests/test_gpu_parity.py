@@ -95,6 +95,28 @@ def test_quant_matches_oracle(cuda, q):
     assert np.array_equal(sse.cpu().numpy(), want_sse)
 
 
+@pytest.mark.parametrize("kind", ["huge", "mixed"])
+def test_quant_custom_tables(cuda, kind):
+    """Tables outside the JPEG-quality family: Q' up to 2^20 (the scalar
+    quantiser's post-shift variant) and an odd/even/1 mix in the packed range."""
+    rng = np.random.default_rng(11 if kind == "huge" else 12)
+    if kind == "huge":
+        qpu = rng.choice([1.0, 7.0, 40000.0, 65536.0, 300001.0, 1048576.0], size=(8, 8))
+    else:
+        qpu = rng.choice([1.0, 2.0, 3.0, 4.0, 6.0, 8.0, 12.0, 16.49, 16.5, 255.0], size=(8, 8))
+    qt = quant.quant_table(qprime_unrounded=qpu)
+    assert qt.wide == (1 if kind == "huge" else 0)
+    x = _imgs(cuda, [21, 22], 128, 256, cfg=2)
+    noise = torch.randint(0, 256, (1, 128, 256), dtype=torch.uint8,
+                          generator=torch.Generator().manual_seed(5)).to(cuda)
+    x = torch.cat([x, noise])
+    rec, sse = batch.compress_quant(x, qt)
+    torch.cuda.synchronize()
+    want_rec, want_sse = exact.compress_quant(x.cpu().numpy(), quant.qtab_qprime(qt))
+    assert np.array_equal(rec.cpu().numpy(), want_rec)
+    assert np.array_equal(sse.cpu().numpy(), want_sse)
+
+
 def test_ragged_width_retain_and_quant(cuda):
     g = torch.Generator().manual_seed(11)
     x = torch.randint(0, 256, (3, 24, 40), dtype=torch.uint8, generator=g)  # W % 16 == 8
