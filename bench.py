@@ -159,6 +159,17 @@ def _ref_forward_task(args):
     return float(refport.coefficient_blocks(img)[0, 0, 0])
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_rate(images, r, budget_s: float, cores: int, task=None):
     """Gpixel/s of the reference algorithm over full `images`, one task per
     worker, for about `budget_s` seconds (task: _ref_task or _ref_quant_task)."""
@@ -260,7 +271,8 @@ def reference_arm(args) -> None:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian blobs + N(0,4^2) noise, BASELINE.json generator)",
         "config": {"workload": cfg["workload"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -472,7 +484,7 @@ def gpu_arm(args) -> None:
             v, info = cpu_reference_rate(sample_imgs, exact.qprime(quant.q50_luma(), q), args.cpu_seconds, cores,
                                          task=_ref_quant_task)
             algo = f"oracle/refport.quant_float64 = reference float64 functions composed (q={q})"
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
                "sample": f"{info['images']} full {info['image_shape'][0]}x{info['image_shape'][1]} config-{args.config} images, "
                          f"one per task on {cores} processes, {info['seconds']:.1f}s; {algo}"}
 
