@@ -133,6 +133,23 @@ int adct_compress_retain(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
                          int32_t r, uint64_t* sse, uint64_t* sse_unrounded,
                          void* stream);
 
+/* adct_compress_retain with the cross-GPU SSE exchange fused into the kernel
+ * epilogue (replaces the separate all-reduce of the SSE
+ * vector).  When the last CTA of image i finishes, it stores the image's
+ * exact SSE into peer_sse[p][peer_offset + i] for every p < n_peers.
+ *   sse        device uint64 [n]: local accumulator (zeroed by the call)
+ *   peer_sse   DEVICE array of n_peers device pointers (symmetric / peer-
+ *              mapped memory, e.g. torch symmetric memory buffer_ptrs_dev),
+ *              each to a uint64 vector with >= peer_offset + n entries
+ *   arrivals   device uint32 [n], zero before the first call; every call
+ *              leaves it zero again
+ * The caller orders peers' reads after every rank's launch (e.g. a stream-
+ * ordered symmetric-memory barrier).  Single plane, rounded SSE only. */
+int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
+                                  int32_t w, int64_t img_stride, int64_t rec_stride, int32_t r,
+                                  uint64_t* sse, uint64_t* const* peer_sse, int32_t n_peers,
+                                  int64_t peer_offset, uint32_t* arrivals, void* stream);
+
 /* ---------------------------------------------------------------------------
  * K3 + K4 — fused quantised compression (single plane batch).
  * Level shift -128, forward T X T^T, quantise by Q' (round half away),

@@ -102,6 +102,41 @@ def compress_retain(
     return rec, sse, ssef
 
 
+def compress_retain_exchange(
+    images: torch.Tensor,
+    r: int,
+    peers_dev: int,
+    n_peers: int,
+    peer_offset: int,
+    arrivals: torch.Tensor,
+    *,
+    reconstruct: bool = True,
+    out: torch.Tensor | None = None,
+    sse_out: torch.Tensor | None = None,
+):
+    """compress_retain whose kernel epilogue also stores each image's exact SSE
+    into every peer's vector: peers_dev is the device address of an array of
+    n_peers device pointers (torch symmetric memory `buffer_ptrs_dev`), image i
+    lands at index peer_offset + i.  `arrivals` is a zeroed int32 [N] scratch
+    tensor that each call leaves zeroed.  Returns (rec | None, local sse[N])."""
+    if not 1 <= int(r) <= 64:
+        raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
+    images = _as_batch(images)
+    n, h, w = images.shape
+    if arrivals.dtype != torch.int32 or arrivals.numel() < n or arrivals.device != images.device:
+        raise ValueError("arrivals must be an int32 tensor of >= N zeros on the images' device")
+    rec = None
+    if reconstruct:
+        rec = out if out is not None else torch.empty_like(images)
+    sse = sse_out if sse_out is not None else torch.empty(n, dtype=torch.int64, device=images.device)
+    _lib.call(
+        "adct_compress_retain_exchange",
+        _ptr(images), _ptr(rec), n, h, w, _img_stride(images), h * w if rec is None else _img_stride(rec),
+        int(r), _ptr(sse), int(peers_dev), int(n_peers), int(peer_offset), _ptr(arrivals), _stream(),
+    )
+    return rec, sse
+
+
 def compress_quant(
     images: torch.Tensor,
     qtab: _lib.QTab,

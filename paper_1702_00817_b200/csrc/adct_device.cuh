@@ -204,10 +204,22 @@ struct PlaneDev {
   uint32_t cta_begin;
 };
 
+// Cross-GPU SSE exchange fused into the retain epilogue (adct_compress_retain_exchange):
+// the CTA that completes an image stores the image's exact SSE into every
+// peer's vector (P2P stores through symmetric / peer-mapped memory).
+struct XchgDev {
+  u64* const* peers;   // device array [n_peers] of peer SSE vectors; nullptr: no exchange
+  u32* arrivals;       // [images] CTA arrival counters, zero between launches
+  int64_t offset;      // this caller's first image in the peers' vectors
+  int32_t n_peers;
+  uint32_t ctas_per_image;
+};
+
 struct PlaneSetDev {
   PlaneDev p[3];
   int32_t n_planes;
   int32_t frame_base;  // first frame of this launch (launches are chunked by 65535 frames)
+  XchgDev x;
 };
 
 // Row words of one unit (8 rows x 16 B, or 8 x 8 B with B-lanes zero).
@@ -333,14 +345,27 @@ __device__ __forceinline__ void cta_sum_init(CtaSum& s) {
   __syncthreads();
 }
 
+// With an exchange descriptor, the CTA's last warp also counts the CTA in
+// for its image (threadfence-reduction pattern); the image's last CTA reads
+// the completed sum and stores it into every peer's vector.
 template <int NT = kThreads>
-__device__ __forceinline__ void cta_sum_add(CtaSum& s, u32 v, u64* dst) {
+__device__ __forceinline__ void cta_sum_add(CtaSum& s, u32 v, u64* sse, int64_t idx, const XchgDev& x) {
   v = __reduce_add_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0) {
     const u64 old = atomicAdd(&s.word, (1ull << 32) | (u64)v);
     if ((u32)(old >> 32) == NT / 32 - 1) {
       const u64 total = (u64)(u32)old + v;
-      if (total != 0) atomicAdd(dst, total);
+      if (total != 0) atomicAdd(sse + idx, total);
+      if (x.peers != nullptr) {
+        __threadfence();
+        if (atomicAdd(x.arrivals + idx, 1u) == x.ctas_per_image - 1) {
+          __threadfence();
+          const u64 image_sse = atomicAdd(sse + idx, 0ull);  // coherent read of the final sum
+          for (int p = 0; p < x.n_peers; ++p) x.peers[p][x.offset + idx] = image_sse;
+          __threadfence_system();
+          x.arrivals[idx] = 0u;  // ready for the next launch
+        }
+      }
     }
   }
 }

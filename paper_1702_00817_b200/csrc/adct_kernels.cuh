@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kRetainThreads) k_retain(PlaneSetDev ps, u64* 
     inv2d(W, U);
     acc = emit_unit<PAIR>(U, w, L.dst, L.width);
   }
-  if (sse != nullptr) cta_sum_add<kRetainThreads>(cta, acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr) cta_sum_add<kRetainThreads>(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x);
 }
 
 // Runtime-r variant: ragged widths (PAIR=false) and the exact "unrounded"
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
   }
-  if (sse != nullptr) cta_sum_add(cta, acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr) cta_sum_add(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x);
   if (FSSE) block_add_u64(accf, ssef + L.frame * ps.n_planes + L.plane);
 }
 

@@ -381,11 +381,15 @@ int adct_forward_int16(const uint8_t* img, int64_t n, int32_t h, int32_t w, int6
 
 // --- K2 retain ---------------------------------------------------------------
 static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, int32_t r,
-                         uint64_t* sse, uint64_t* ssef, void* stream) {
+                         uint64_t* sse, uint64_t* ssef, void* stream, const XchgDev* xchg = nullptr) {
   if (r < 1 || r > 64) return ADCT_ERR_INVALID_RETENTION;
   PlaneSetHost ps;
   int rc = build_planes(planes, n_planes, n_frames, ps);
   if (rc != ADCT_OK) return rc;
+  if (xchg != nullptr) {  // single plane, no unrounded SSE (checked by the caller)
+    ps.dev.x = *xchg;
+    ps.dev.x.ctas_per_image = (uint32_t)ps.grid_x;
+  }
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
@@ -396,6 +400,10 @@ static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n
     PlaneSetHost ps128;  // the pruned retain kernels run 128-unit tiles
     rc = build_planes(planes, n_planes, n_frames, ps128, false, kRetainThreads);
     if (rc != ADCT_OK) return rc;
+    if (xchg != nullptr) {
+      ps128.dev.x = *xchg;
+      ps128.dev.x.ctas_per_image = (uint32_t)ps128.grid_x;
+    }
     RetainKernel k = retain_kernel(r);
     return for_frame_chunks(ps128, n_frames, [&](dim3 g) { k<<<g, kRetainThreads, 0, s>>>(ps128.dev, d_sse); });
   }
@@ -416,6 +424,25 @@ int adct_compress_retain(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
   if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
   adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
   return retain_planes(&pl, 1, n, r, sse, sse_unrounded, stream);
+}
+
+int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h, int32_t w,
+                                  int64_t img_stride, int64_t rec_stride, int32_t r, uint64_t* sse,
+                                  uint64_t* const* peer_sse, int32_t n_peers, int64_t peer_offset,
+                                  uint32_t* arrivals, void* stream) {
+  if (n < 0 || n_peers < 1 || n_peers > 1024 || peer_offset < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (r < 1 || r > 64) return ADCT_ERR_INVALID_RETENTION;
+  if (n == 0) return ADCT_OK;  // nothing to compute or exchange
+  if (sse == nullptr || peer_sse == nullptr || arrivals == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (!aligned(sse, 8) || !aligned(peer_sse, 8) || !aligned(arrivals, 4)) return ADCT_ERR_MISALIGNED;
+  XchgDev x;
+  x.peers = reinterpret_cast<u64* const*>(peer_sse);
+  x.arrivals = arrivals;
+  x.offset = peer_offset;
+  x.n_peers = n_peers;
+  x.ctas_per_image = 0;  // set from the launch geometry
+  adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
+  return retain_planes(&pl, 1, n, r, sse, nullptr, stream, &x);
 }
 
 int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,

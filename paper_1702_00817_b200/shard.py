@@ -2,10 +2,16 @@
 
 Images (or video frames) are independent, so rank k of N owns the contiguous
 range [k*n/N, (k+1)*n/N) and runs the fused kernel on it with no data-path
-communication.  The only exchange is one all-reduce(SUM) of the per-image
-int64 SSE vector (each rank fills its slice, zeros elsewhere), after which
-every rank holds the exact global SSE and PSNR — bit-identical for any N
-because integer sums are order independent.
+communication.  The only exchange is the per-image int64 SSE vector, after
+which every rank holds the exact global SSE and PSNR — bit-identical for any
+N because integer sums are order independent.  Two ways to exchange it:
+
+* `global_sse` / `run_sharded`: one all-reduce(SUM) (each rank fills its
+  slice, zeros elsewhere) — NCCL over NVLink.
+* `SseExchange`: the retain kernel's epilogue stores each
+  finished image's SSE straight into every rank's symmetric-memory vector
+  (P2P over NVLink), then one stream-ordered symmetric-memory barrier; no
+  collective launch.
 
 torch.distributed is the plumbing: NCCL over NVLink/NVSwitch on the B200 box,
 gloo on CPU for the multi-rank tests.
@@ -95,3 +101,41 @@ def run_sharded(
     if local.shape[0] != sh.count:
         raise ValueError(f"compute returned {local.shape[0]} rows for a shard of {sh.count}")
     return global_sse(local, sh, n_total, group)
+
+
+class SseExchange:
+    """Global SSE vector in torch symmetric memory, filled by the fused
+    retain kernel's epilogue on every rank (adct_compress_retain_exchange).
+
+        ex = SseExchange(n_total, device)
+        rec, local = ex.compress_retain(images_of_this_rank, r, shard.start)
+        ex.sse  # int64 [n_total], identical on every rank after the call
+    """
+
+    def __init__(self, n_total: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if not dist.is_initialized():
+            raise RuntimeError("SseExchange needs an initialised process group (NCCL)")
+        group = group or dist.group.WORLD
+        self.n_total = int(n_total)
+        self.sse = symm_mem.empty(self.n_total, dtype=torch.int64, device=device)
+        self.sse.zero_()
+        self._hdl = symm_mem.rendezvous(self.sse, group.group_name)
+        self.n_peers = int(self._hdl.world_size)
+        self._arrivals: torch.Tensor | None = None
+
+    def compress_retain(self, images: torch.Tensor, r: int, offset: int, *, out=None, sse_out=None):
+        from . import batch
+
+        n = images.shape[0] if images.dim() == 3 else 1
+        if offset < 0 or offset + n > self.n_total:
+            raise ValueError(f"images [{offset}, {offset + n}) outside the exchange vector of {self.n_total}")
+        if self._arrivals is None or self._arrivals.numel() < n:
+            self._arrivals = torch.zeros(max(n, 1), dtype=torch.int32, device=images.device)
+        rec, local = batch.compress_retain_exchange(
+            images, r, self._hdl.buffer_ptrs_dev, self.n_peers, offset, self._arrivals, out=out, sse_out=sse_out
+        )
+        self._hdl.barrier(channel=0)  # stream-ordered: every rank's pushes are visible after this
+        return rec, local
+

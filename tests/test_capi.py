@@ -173,6 +173,18 @@ def test_entry_points_validate_before_any_cuda_call():
     assert L.adct_compress_quant(n, n, 1, 64, 64, 4096, 4096, ctypes.byref(bad), n, n) == 3
     planes = (_lib.Plane * 4)()
     assert L.adct_compress_quant_planes(planes, 4, 1, ctypes.byref(qt), n, n) == 5
+    # fused SSE exchange: missing accumulator / peers / counters, bad peer count or offset
+    p8 = ctypes.c_void_p(0x1000)
+    X = L.adct_compress_retain_exchange
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, n, p8, 1, 0, p8, n) == 5
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, p8, n, 1, 0, p8, n) == 5
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, p8, p8, 1, 0, n, n) == 5
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, p8, p8, 0, 0, p8, n) == 5
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, p8, p8, 1, -1, p8, n) == 5
+    assert X(n, n, 1, 64, 64, 4096, 4096, 10, ctypes.c_void_p(0x1004), p8, 1, 0, p8, n) == 6
+    assert X(n, n, 1, 64, 64, 4096, 4096, 0, p8, p8, 1, 0, p8, n) == 2
+    assert X(n, n, 0, 64, 64, 4096, 4096, 10, p8, p8, 1, 0, p8, n) == 0
+    assert X(n, n, 0, 64, 64, 4096, 4096, 10, n, n, 1, 0, n, n) == 0  # empty call: nothing touched
 
 
 def test_error_mapping():

@@ -1,0 +1,84 @@
+"""the SSE exchange fused into the retain kernel epilogue.
+
+On one GPU the multi-peer push is exercised with several local vectors as
+the "peers" (no kernel waits on another), and the torch symmetric-memory
+wrapper (`shard.SseExchange`) at world size 1 in a child process.  Results
+must equal adct_compress_retain's exact SSE."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1702_00817_b200 import batch, synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _peer_array(vectors):
+    ptrs = torch.tensor([v.data_ptr() for v in vectors], dtype=torch.int64, device=vectors[0].device)
+    return ptrs
+
+
+@pytest.mark.parametrize("shape", [(6, 64, 256), (5, 40, 24), (3, 256, 2048)])
+def test_exchange_matches_retain_on_local_peers(cuda, shape):
+    n, h, w = shape
+    x = synth.images_device(range(40, 40 + n), h, w, 16, 8.0, 64.0, device=cuda)
+    rec_ref, sse_ref, _ = batch.compress_retain(x, 10)
+    offset, total = 7, n + 11
+    peers = [torch.full((total,), -5, dtype=torch.int64, device=cuda) for _ in range(3)]
+    ptrs = _peer_array(peers)
+    arrivals = torch.zeros(n, dtype=torch.int32, device=cuda)
+    for rep in range(2):  # counters are left at zero, so the call repeats
+        for v in peers:
+            v.fill_(-5)
+        rec, local = batch.compress_retain_exchange(x, 10, ptrs.data_ptr(), len(peers), offset, arrivals)
+        torch.cuda.synchronize()
+        assert torch.equal(rec, rec_ref) and torch.equal(local, sse_ref)
+        for v in peers:
+            assert torch.equal(v[offset:offset + n], sse_ref)
+            assert bool((v[:offset] == -5).all()) and bool((v[offset + n:] == -5).all())
+        assert int(arrivals.abs().sum()) == 0
+
+
+def test_exchange_reconstruct_off_and_zero_images(cuda):
+    x = synth.images_device(range(3), 128, 128, 16, 8.0, 64.0, device=cuda)
+    _, sse_ref, _ = batch.compress_retain(x, 3)
+    peer = torch.zeros(3, dtype=torch.int64, device=cuda)
+    ptrs = _peer_array([peer])
+    arrivals = torch.zeros(3, dtype=torch.int32, device=cuda)
+    rec, local = batch.compress_retain_exchange(x, 3, ptrs.data_ptr(), 1, 0, arrivals, reconstruct=False)
+    torch.cuda.synchronize()
+    assert rec is None and torch.equal(peer, sse_ref) and torch.equal(local, sse_ref)
+    e = x[:0]
+    _, local0 = batch.compress_retain_exchange(e, 3, ptrs.data_ptr(), 1, 0, arrivals)
+    assert local0.numel() == 0
+
+
+def test_symmetric_memory_exchange_world1(cuda):
+    """shard.SseExchange end to end (NCCL process group of one rank)."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29541", RANK="0", WORLD_SIZE="1",
+               LOCAL_RANK="0", PYTHONPATH=ROOT)
+    code = r'''
+import torch, torch.distributed as dist
+from paper_1702_00817_b200 import batch, shard, synth
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+x = synth.images_device(range(9), 256, 256, 16, 8.0, 64.0, device="cuda")
+_, want, _ = batch.compress_retain(x, 10)
+ex = shard.SseExchange(12, "cuda")
+for rep in range(2):
+    rec, local = ex.compress_retain(x[:5], 10, 0)
+    rec2, local2 = ex.compress_retain(x[5:], 10, 5)
+    torch.cuda.synchronize()
+    assert torch.equal(ex.sse[:9], want), (ex.sse, want)
+    assert int(ex.sse[9:].abs().sum()) == 0
+dist.destroy_process_group()
+print("EXCHANGE_OK")
+'''
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert "EXCHANGE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
