@@ -45,7 +45,8 @@ struct PlaneSetHost {
 // block per thread (used by k_quant_wide).
 int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, PlaneSetHost& out,
                  bool force_single = false, int tile = kThreads) {
-  if (planes == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
+  // frames are indexed as int32 inside a launch (frame_base + blockIdx.y)
+  if (planes == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0 || n_frames > 0x7FFFFFFF)
     return ADCT_ERR_INVALID_ARGUMENT;
   std::memset(&out.dev, 0, sizeof(out.dev));
   bool pair = !force_single;
@@ -79,7 +80,8 @@ int build_planes(const adct_plane_t* planes, int n_planes, int64_t n_frames, Pla
     d.units = d.upr * (uint32_t)(p.height / 8);
     d.upr_magic = 0;  // 0 encodes upr == 1 (brow = unit)
     if (d.units > 0 && d.upr > 1) {
-      // unit / upr as one multiply-high; exhaustively verified (units <= 2^26 here)
+      // unit / upr as one multiply-high, verified at every block-row start and
+      // the unit before it (both sides are monotone step functions of unit)
       const uint64_t m = (0x100000000ull + d.upr - 1) / d.upr;
       if (m > 0xFFFFFFFFull) return ADCT_ERR_INVALID_ARGUMENT;
       d.upr_magic = (uint32_t)m;

@@ -185,6 +185,7 @@ def test_entry_points_validate_before_any_cuda_call():
     assert X(n, n, 1, 64, 64, 4096, 4096, 0, p8, p8, 1, 0, p8, n) == 2
     assert X(n, n, 0, 64, 64, 4096, 4096, 10, p8, p8, 1, 0, p8, n) == 0
     assert X(n, n, 0, 64, 64, 4096, 4096, 10, n, n, 1, 0, n, n) == 0  # empty call: nothing touched
+    assert L.adct_compress_retain(n, n, 2**31, 8, 8, 64, 64, 10, n, n, n) == 5  # > 2^31 frames
 
 
 def test_error_mapping():
