@@ -172,6 +172,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 // cost).  Each thread only touches its own smem slots, so the ring needs no
 // CTA barrier; cp.async.wait_group is per thread.
 // ---------------------------------------------------------------------------
+#ifndef ADCT_QP_MINB
+#define ADCT_QP_MINB 2  // resident CTAs per SM for k_quant_p (register budget 128)
+#endif
 struct TileCursor {
   int plane;
   int64_t frame;
@@ -227,7 +230,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <bool PAIR, bool FLIP>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
   extern __shared__ uint4 s_ring[];  // [2][8][kThreads]

@@ -131,12 +131,12 @@ int for_frame_chunks(PlaneSetHost& ps, int64_t n_frames, F&& launch) {
   return ADCT_OK;
 }
 
-// Persistent kernels: 2 CTAs of 256 threads per SM.
+// Persistent kernels: ADCT_QP_MINB (2) CTAs of 256 threads per SM.
 int persistent_grid(int* grid) {
   int dev = 0, sms = 0;
   ADCT_CUDA_TRY(cudaGetDevice(&dev));
   ADCT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  *grid = 2 * sms;
+  *grid = ADCT_QP_MINB * sms;
   return ADCT_OK;
 }
 
