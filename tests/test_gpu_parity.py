@@ -146,6 +146,30 @@ def test_planes_quant_one_launch(cuda):
         assert np.array_equal(sse[:, k].cpu().numpy(), ws)
 
 
+@pytest.mark.parametrize("r", [1, 10, 64])
+def test_planes_retain_one_launch(cuda, r):
+    """adct_compress_retain_planes: Y + Cb + Cr (one plane with a width that
+    cannot pair) in one launch, per-frame per-plane SSE."""
+    g = torch.Generator().manual_seed(6 + r)
+    y = torch.randint(0, 256, (3, 72, 128), dtype=torch.uint8, generator=g)
+    cb = torch.randint(0, 256, (3, 40, 64), dtype=torch.uint8, generator=g)
+    cr = torch.randint(0, 256, (3, 40, 64), dtype=torch.uint8, generator=g)
+    recs, sse = batch.compress_retain_planes([y.to(cuda), cb.to(cuda), cr.to(cuda)], r)
+    torch.cuda.synchronize()
+    for k, p in enumerate((y, cb, cr)):
+        wr, ws, _ = exact.compress_retain(p.numpy(), r)
+        assert np.array_equal(recs[k].cpu().numpy(), wr)
+        assert np.array_equal(sse[:, k].cpu().numpy(), ws)
+    y2 = torch.randint(0, 256, (2, 16, 24), dtype=torch.uint8, generator=g)  # 24 px: single-block units
+    c2 = torch.randint(0, 256, (2, 8, 16), dtype=torch.uint8, generator=g)
+    recs2, sse2 = batch.compress_retain_planes([y2.to(cuda), c2.to(cuda)], r)
+    torch.cuda.synchronize()
+    for k, p in enumerate((y2, c2)):
+        wr, ws, _ = exact.compress_retain(p.numpy(), r)
+        assert np.array_equal(recs2[k].cpu().numpy(), wr)
+        assert np.array_equal(sse2[:, k].cpu().numpy(), ws)
+
+
 def test_sweep_matches_oracle(cuda):
     x = _imgs(cuda, [0, 1, 2], 128, 128)
     s = batch.sweep_retain_sse(x, 1, 45)
