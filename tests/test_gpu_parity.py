@@ -148,8 +148,8 @@ def test_planes_quant_one_launch(cuda):
 
 @pytest.mark.parametrize("r", [1, 10, 64])
 def test_planes_retain_one_launch(cuda, r):
-    """adct_compress_retain_planes: Y + Cb + Cr (one plane with a width that
-    cannot pair) in one launch, per-frame per-plane SSE."""
+    """adct_compress_retain_planes: Y + Cb + Cr in one launch with per-frame,
+    per-plane SSE; then planes whose 24-px width cannot pair blocks."""
     g = torch.Generator().manual_seed(6 + r)
     y = torch.randint(0, 256, (3, 72, 128), dtype=torch.uint8, generator=g)
     cb = torch.randint(0, 256, (3, 40, 64), dtype=torch.uint8, generator=g)
