@@ -374,6 +374,101 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K7, incremental form (rounded SSE only): the inverse is linear, so going
+// from r-1 to r kept coefficients adds one basis image,
+//   64 X += E_uv Z_uv T[u]^T T[v]      ((u, v) = zigzag position r-1),
+// i.e. 8 + 64 multiply-adds with factors in {-1, 0, 1} from a uniform table
+// instead of 64 masks + a full 224-add inverse.  The E-scaled coefficients
+// wait in shared memory (their index is the runtime zigzag position).
+// ---------------------------------------------------------------------------
+#ifdef ADCT_DEFINE_PLAIN_KERNELS  // one __constant__ copy: defined in capi.cu only
+constexpr int kSweepThreads = 128;
+
+struct SweepTables {
+  int4 t[8][2];   // rows of T, t[u][h] = T[u][4h .. 4h+3]
+  int zz[64];     // zigzag rank -> u*8+v
+};
+__host__ __device__ constexpr SweepTables make_sweep_tables() {
+  SweepTables s{};
+  for (int u = 0; u < 8; ++u)
+    for (int h = 0; h < 2; ++h) {
+      s.t[u][h].x = t_entry(u, 4 * h);
+      s.t[u][h].y = t_entry(u, 4 * h + 1);
+      s.t[u][h].z = t_entry(u, 4 * h + 2);
+      s.t[u][h].w = t_entry(u, 4 * h + 3);
+    }
+  for (int k = 0; k < 64; ++k) s.zz[k] = zz_pos(k);
+  return s;
+}
+__constant__ SweepTables c_sweep = make_sweep_tables();
+
+template <bool PAIR>
+__global__ void __launch_bounds__(kSweepThreads)
+    k_sweep_inc(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse) {
+  __shared__ u32 zs[64][kSweepThreads];
+  UnitLoc L;
+  const bool active = locate_unit<PAIR, kSweepThreads>(ps, L);
+  uint4 w[8];
+  if (active) {
+    u32 x[8][8], Z[8][8];
+    load_unit<PAIR>(L.src, L.width, w);
+    unpack_unit(w, x);
+    fwd2d(x, Z);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) zs[u * 8 + v][threadIdx.x] = Z[u][v] << (e_log2(u) + e_log2(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int p = 0; p < 64; ++p) zs[p][threadIdx.x] = 0u;
+  }
+  u32 U[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) U[i][j] = kDcRound;  // T^T (kDcRound e0 e0^T) T = kDcRound everywhere
+  const int nr = r_max - r_min + 1;
+  u64* out = sse + L.frame * nr;
+#pragma unroll 1
+  for (int r = 1; r <= r_max; ++r) {
+    const int p = c_sweep.zz[r - 1];
+    const int u = p >> 3, v = p & 7;
+    const u32 z = zs[p][threadIdx.x];
+    const int4 a0 = c_sweep.t[u][0], a1 = c_sweep.t[u][1];
+    const int4 b0 = c_sweep.t[v][0], b1 = c_sweep.t[v][1];
+    const int a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const int b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    u32 bz[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bz[j] = z * (u32)b[j];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) U[i][j] += (u32)a[i] * bz[j];
+    if (r >= r_min) {
+      u32 acc = 0;
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint4 o;
+          pack_row(U[i], o);
+          acc = sse4(w[i].x, o.x, acc);
+          acc = sse4(w[i].y, o.y, acc);
+          if (PAIR) {
+            acc = sse4(w[i].z, o.z, acc);
+            acc = sse4(w[i].w, o.w, acc);
+          }
+        }
+      }
+      block_add_u32(acc, out + (r - r_min));
+    }
+  }
+}
+#endif  // ADCT_DEFINE_PLAIN_KERNELS
+
+// ---------------------------------------------------------------------------
 // K1: forward integer transform, coefficients in _tile order.
 // The output block of unit u is 2u (pair) or u, so a warp's output is one
 // contiguous run of 32 units x 2 blocks.  Each thread writes one block at a

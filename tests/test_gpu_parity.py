@@ -170,6 +170,40 @@ def test_planes_retain_one_launch(cuda, r):
         assert np.array_equal(sse2[:, k].cpu().numpy(), ws)
 
 
+@pytest.mark.parametrize("shape,r_min,r_max", [((3, 40, 24), 1, 64), ((2, 72, 144), 7, 30),
+                                               ((5, 16, 2048), 64, 64), ((1, 8, 8), 2, 2)])
+@pytest.mark.parametrize("kernel", ["inc", "full"])
+def test_sweep_shapes_and_ranges(cuda, shape, r_min, r_max, kernel):
+    """Both sweep kernels (incremental basis updates / full masked inverse,
+    selected by ADCT_SWEEP_KERNEL in a child process) over unpaired widths,
+    partial CTAs, r ranges not starting at 1, and a single r."""
+    import os
+    import subprocess
+    import sys
+
+    g = torch.Generator().manual_seed(sum(shape) + r_min)
+    x = torch.randint(0, 256, shape, dtype=torch.uint8, generator=g)
+    want = exact.sweep_sse(x.numpy(), r_min, r_max)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch\n"
+        "from paper_1702_00817_b200 import batch\n"
+        "x = torch.from_numpy(np.load(sys.argv[1])).cuda()\n"
+        f"s = batch.sweep_retain_sse(x, {r_min}, {r_max})\n"
+        "np.save(sys.argv[2], s.cpu().numpy())\n"
+    )
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "x.npy"), x.numpy())
+        env = dict(os.environ, ADCT_SWEEP_KERNEL=kernel, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code, os.path.join(td, "x.npy"), os.path.join(td, "s.npy")],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-3000:]
+        got = np.load(os.path.join(td, "s.npy"))
+    assert np.array_equal(got, want)
+
+
 def test_sweep_matches_oracle(cuda):
     x = _imgs(cuda, [0, 1, 2], 128, 128)
     s = batch.sweep_retain_sse(x, 1, 45)
