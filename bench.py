@@ -457,27 +457,38 @@ def gpu_arm(args) -> None:
         try:
             with HostPipeline(local, chunk_bytes=args.e2e_chunk_mb << 20) as pipe:
                 if cfg["kind"] == "retain":
-                    call = lambda: pipe.compress_retain(host_in, cfg["r"], host_out, register=False)
+                    call = lambda rec: pipe.compress_retain(host_in, cfg["r"], rec, register=False)
                 else:
                     qt0 = quant.quant_table(cfg["q"][0])
-                    call = lambda: pipe.compress_quant(host_in, qt0, host_out, register=False)
-                call()
-                reps = 3
-                if world > 1:
-                    dist.barrier()
-                t0 = time.perf_counter()
-                for _ in range(reps):
-                    call()
-                dt = (time.perf_counter() - t0) / reps
-            if world > 1:
-                t = torch.tensor([dt], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                dt = t.item()
-            e2e = {"value": world * m * cfg["h"] * cfg["w"] / dt / 1e9, "unit": UNIT,
+                    call = lambda rec: pipe.compress_quant(host_in, qt0, rec, register=False)
+
+                def timed(rec):
+                    call(rec)
+                    reps = 3
+                    if world > 1:
+                        dist.barrier()
+                    t0 = time.perf_counter()
+                    for _ in range(reps):
+                        call(rec)
+                    dt = (time.perf_counter() - t0) / reps
+                    if world > 1:
+                        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                        dt = t.item()
+                    return dt
+
+                dt = timed(host_out)  # reconstructions come back to the host every step
+                dt_metric = timed(None)  # inputs in, per-image SSE (-> PSNR) back
+            px = world * m * cfg["h"] * cfg["w"]
+            e2e = {"value": px / dt / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": int(world * host_in.nbytes),
                    "d2h_bytes_per_step": int(world * (host_out.nbytes + 8 * m)),
                    "images_per_step": world * m,
-                   "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks"}
+                   "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks",
+                   "metric_only": {"value": px / dt_metric / 1e9, "unit": UNIT,
+                                   "h2d_bytes_per_step": int(world * host_in.nbytes),
+                                   "d2h_bytes_per_step": int(world * 8 * m),
+                                   "note": "reconstructions kept on the device; only the SSE/PSNR vector is read back"}}
         finally:
             del host_in, host_out
 
