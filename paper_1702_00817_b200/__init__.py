@@ -39,7 +39,7 @@ from .errors import (
 )
 from .flowgraph import OpCount, count_operations, fast_forward, flow_intermediates
 from .metrics import CorpusSummary, QualityRecord, ape_vs_dct, mse, psnr, summarize
-from .sweep import ExperimentConfig, run_sweep, write_sweep_outputs
+from .sweep import ExperimentConfig, compare_transforms, run_sweep, write_sweep_outputs
 from .transforms import (
     ApproximateTransform,
     DiagonalScaling,

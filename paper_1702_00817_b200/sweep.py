@@ -14,6 +14,9 @@ The loop over images and r is replaced by one launch per image batch:
 
 `write_sweep_outputs` writes records.csv, summary.csv and run_metadata.json in
 the reference's format (cli.py:127-152, metrics.py:100-122).
+
+`compare_transforms` is the GPU form of cli.cmd_lena (cli.py:187-204): one
+image, one r, PSNR per transform and optionally the reconstructions as PGM.
 """
 
 from __future__ import annotations
@@ -158,3 +161,29 @@ def write_sweep_outputs(out_dir, config: ExperimentConfig, records, summaries, a
     with open(out / "run_metadata.json", "w") as fp:
         json.dump(meta, fp, indent=2, sort_keys=True)
         fp.write("\n")
+
+
+def compare_transforms(image, r: int, transforms_=("dct", "proposed"), *, out_dir=None, stem: str = "image"):
+    """PSNR of every transform's retain-r reconstruction of one image, in the
+    order given (cli.cmd_lena, cli.py:187-204: reference float semantics,
+    unrounded clamped reconstruction, metrics.mse + metrics.psnr).  With
+    `out_dir`, each reconstruction is written as `<stem>_<name>_r<r>.pgm`
+    (samples rounded half away, corpus.write_pgm).  Registry transforms are
+    passed as objects.  Returns [(name, psnr_db)]."""
+    from . import pgm
+
+    img = np.asarray(image)
+    if out_dir is not None:
+        out_dir = Path(out_dir)
+        out_dir.mkdir(parents=True, exist_ok=True)
+    rows = []
+    for t in transforms_:
+        tr = resolve_transform(t)
+        recon = np.asarray(codec.compress_image(tr, img, r))
+        value = metrics.psnr(metrics.mse(img, recon))
+        rows.append((_name(t), value))
+        if out_dir is not None:
+            h, w = recon.shape
+            pgm.write_pgm(pgm.GrayImage(w, h, recon), out_dir / f"{stem}_{_name(t)}_r{r}.pgm")
+    return rows
+

@@ -95,6 +95,28 @@ def test_run_sweep_matches_reference_semantics(cuda, tmp_path):
     assert json.load(open(tmp_path / "run_metadata.json"))["psnr_convention"] == "mean_of_per_image_psnr"
 
 
+def test_compare_transforms_is_cmd_lena(cuda, tmp_path):
+    """sweep.compare_transforms = cli.cmd_lena: PSNR per transform at one r
+    (reference float semantics) and the reconstructions as P5 files."""
+    from paper_1702_00817_b200 import pgm
+
+    img = IMAGES["c1_seed1_128"]
+    reg = transforms.ApproximateTransform(transforms.TransformMatrix("flipped", -exact.T),
+                                          transforms.derive_scaling(transforms.TransformMatrix("flipped", -exact.T)))
+    rows = sweep.compare_transforms(img, 25, ("dct", "proposed", reg), out_dir=tmp_path, stem="c1")
+    assert [n for n, _ in rows] == ["dct", "proposed", "flipped"]
+    prop = transforms.proposed_transform()
+    for (name, value), C in zip(rows, (DCT.matrix, prop.matrix, reg.matrix)):
+        want = ref_sweep_mse(C, np.asarray(img, dtype=np.float64), [25])[0]
+        assert value == pytest.approx(metrics.psnr(want), abs=1e-8)
+        f = tmp_path / f"c1_{name}_r25.pgm"
+        g = pgm.read_pgm(f)
+        recon = np.asarray(codec.compress_image(sweep.resolve_transform(
+            {"dct": "dct", "proposed": "proposed"}.get(name, reg)), img, 25))
+        assert np.array_equal(np.asarray(g.samples), np.floor(recon + 0.5))
+    assert rows[1][1] == pytest.approx(rows[2][1], abs=1e-9)  # -T gives the same reconstruction
+
+
 def test_registry_style_transform_object(cuda):
     """Any object with an 8x8 .matrix works (e.g. a reference registry kernel)."""
     k = exact.T.astype(np.float64)
