@@ -238,9 +238,11 @@ int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w,
                      const uint64_t* noise_seed, void* stream);
 
 /* ---------------------------------------------------------------------------
- * Host-buffer pipeline (the end-to-end entry point).  Streams batches of
- * host images through the device in chunks: H2D copy of chunk i+1, fused
- * compress of chunk i and D2H copy of chunk i-1 overlap on separate streams.
+ * Host-buffer pipeline (the end-to-end entry point).  Replaces the host-side
+ * per-image loop of the reference (numpy images from corpus.read_pgm,
+ * corpus.py:65-111, each through compress_image + mse, cli.py:101-113) for
+ * whole batches: H2D copy of chunk i+1, fused compress of chunk i and D2H
+ * copy of chunk i-1 overlap on separate streams.
  * Host buffers should be pinned for full speed: adct_host_alloc memory
  * (cudaHostAlloc) reaches the PCIe limit; adct_host_register'd memory runs
  * ~9 % slower on the B200 boxes measured (tools/pcie_probe2.py).
