@@ -551,6 +551,104 @@ __global__ void __launch_bounds__(kForwardThreads)
 }
 
 #ifdef ADCT_DEFINE_PLAIN_KERNELS  // non-template kernels: defined once, in capi.cu
+// K3 for coarse tables whose quantiser still fits 16-bit lanes (every
+// Q' <= 8191, e.g. q = 10): the forward transform and the two-lane quantiser
+// run packed for two blocks (exact: |Z| <= 8192), dequantisation goes to
+// int32 per block, and only the inverse — the part whose range needs more
+// than 16 bits — runs per block in 32 bits.  Block A's column inverse
+// streams in registers; block B's dequantised coefficients wait in shared
+// memory.  `q.wadd` holds the scalar offsets here (-kq*qe, + 32 + 8192 at DC).
+__device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
+  u32 h2[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int a = V[4 * half + 2 * j] >> 6, b = V[4 * half + 2 * j + 1] >> 6;  // |.| < 2^15
+    h2[j] = __vimin_s16x2_relu(__byte_perm((u32)a, (u32)b, 0x5410), 0x00FF00FFu);
+  }
+  return __byte_perm(h2[0], h2[1], 0x6420);
+}
+
+constexpr size_t kHybridSmem = (size_t)64 * kThreads * sizeof(int) + (size_t)8 * kThreads * sizeof(uint4);
+
+__global__ void __launch_bounds__(kThreads, 2)
+    k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
+  extern __shared__ uint4 s_dyn[];
+  uint4* s_orig = s_dyn;                                          // [8][kThreads]
+  int* s_wb = reinterpret_cast<int*>(s_dyn + 8 * kThreads);       // [64][kThreads]
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<true>(ps, L)) {
+    uint4 w[8];
+    load_unit<true>(L.src, L.width, w);
+    u32 x[8][8];
+    unpack_unit(w, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_orig[i * kThreads + threadIdx.x] = w[i];
+    int cA[8][8];
+    {
+      u32 t[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        u32 col[8], Zc[8];
+        int wa[8], cc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+        fwd8(col, Zc);
+        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int p = u * 8 + v;
+          const uint4 c = q.pos[p];
+          const u32 z = Zc[u];
+          const u32 sg = ((z >> 15) & 0x10001u) ^ 0x10001u;
+          const u32 U = z * c.y + c.z + sg;
+          const u32 qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
+          const u32 qb = __umulhi(U >> 16, c.x);      // lane B
+          wa[u] = (int)(qa * c.w) + (int)q.wadd[p];
+          s_wb[p * kThreads + threadIdx.x] = (int)(qb * c.w) + (int)q.wadd[p];
+        }
+        inv8(wa, cc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cA[i][v] = cc[i];
+      }
+    }
+    // block A rows go out now (8-byte stores; L2 merges them with B's halves)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int V[8];
+      inv8(cA[i], V);
+      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
+      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width, o);
+      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      acc = sse4(wi.x, o.x, acc);
+      acc = sse4(wi.y, o.y, acc);
+    }
+    int cB[8][8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      int col[8], cc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) col[u] = s_wb[(u * 8 + v) * kThreads + threadIdx.x];
+      inv8(col, cc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cB[i][v] = cc[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int V[8];
+      inv8(cB[i], V);
+      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
+      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width + 8, o);
+      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      acc = sse4(wi.z, o.x, acc);
+      acc = sse4(wi.w, o.y, acc);
+    }
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+}
+
 // K3 for coarse tables (wide == 1, e.g. q < 25): one block per thread.  The
 // B lane is empty, so the "linear form" is a plain int32 and every
 // intermediate is exact whatever its magnitude.

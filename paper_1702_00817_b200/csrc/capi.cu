@@ -172,6 +172,30 @@ QParamsDev to_qparams(const adct_qtab_t& t) {
   return q;
 }
 
+// Packed quantiser + scalar dequantiser (k_quant_hybrid); false when some
+// position's Q' is beyond the two-lane quantiser (mult == 0).
+bool to_qparams_hybrid(const adct_qtab_t& t, QParamsDev* q) {
+  for (int p = 0; p < 64; ++p) {
+    if (t.mult[p] == 0) return false;
+    q->pos[p].x = t.magic[p];
+    q->pos[p].y = (uint32_t)t.mult[p];
+    q->pos[p].z = (uint32_t)t.bias[p] * (uint32_t)t.mult[p] * 65537u;
+    q->pos[p].w = (uint32_t)t.qe[p];
+    q->wadd[p] = (uint32_t)0 - (uint32_t)t.kq[p] * (uint32_t)t.qe[p];
+  }
+  q->wadd[0] += 32u + 8192u;  // rounding, +128 back (64 * 128)
+  return true;
+}
+
+// ADCT_WIDE_KERNEL = scalar forces k_quant_wide for every coarse table (A/B).
+int wide_kernel_choice() {
+  static const int v = [] {
+    const char* e = std::getenv("ADCT_WIDE_KERNEL");
+    return (e && std::strcmp(e, "scalar") == 0) ? 0 : 1;
+  }();
+  return v;
+}
+
 QParamsWide to_qparams_wide(const adct_qtab_t& t) {
   QParamsWide q;
   for (int p = 0; p < 64; ++p) {
@@ -477,6 +501,19 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
   u64* d_sse = reinterpret_cast<u64*>(sse);
   if (wide) {
+    QParamsDev qh;
+    if (wide_kernel_choice() == 1 && to_qparams_hybrid(*qtab, &qh)) {
+      PlaneSetHost ph;  // two blocks per thread where every plane pairs
+      rc = build_planes(planes, n_planes, n_frames, ph, false);
+      if (rc != ADCT_OK) return rc;
+      if (ph.pair) {
+        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kHybridSmem));
+        return for_frame_chunks(ph, n_frames, [&](dim3 g) {
+          k_quant_hybrid<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
+        });
+      }
+    }
     const QParamsWide qw = to_qparams_wide(*qtab);
     return for_frame_chunks(ps, n_frames, [&](dim3 g) { k_quant_wide<<<g, kThreads, 0, s>>>(ps.dev, qw, d_sse); });
   }
