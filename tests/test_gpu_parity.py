@@ -215,3 +215,40 @@ def test_empty_batch(cuda):
     x = torch.empty((0, 64, 64), dtype=torch.uint8, device=cuda)
     rec, sse, _ = batch.compress_retain(x, 10)
     assert rec.shape == (0, 64, 64) and sse.shape == (0,)
+
+
+@pytest.mark.parametrize("env", [{"ADCT_QUANT_KERNEL": "grid"}, {"ADCT_WIDE_KERNEL": "scalar"},
+                                 {"ADCT_PIPELINE_DEPTH": "2"}])
+def test_alternate_kernel_paths(cuda, env):
+    """The A/B switches keep their kernels exact: one-tile-per-CTA quant
+    kernel, scalar coarse-table kernel, a 2-deep host pipeline (child process:
+    the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+from oracle import exact
+from paper_1702_00817_b200 import batch, quant
+from paper_1702_00817_b200.pipeline import HostPipeline
+g = torch.Generator().manual_seed(3)
+for shape in ((3, 64, 256), (2, 40, 24)):
+    x = torch.randint(0, 256, shape, dtype=torch.uint8, generator=g)
+    for q in (10, 30, 75):
+        qt = quant.quant_table(q)
+        rec, sse = batch.compress_quant(x.cuda(), qt)
+        wr, ws = exact.compress_quant(x.numpy(), quant.qtab_qprime(qt))
+        assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws), (shape, q)
+    with HostPipeline(0, chunk_bytes=1 << 15) as p:
+        out = np.empty(shape, np.uint8)
+        _, s2 = p.compress_retain(x.numpy(), 10, out)
+        wr, ws, _ = exact.compress_retain(x.numpy(), 10)
+        assert np.array_equal(out, wr) and np.array_equal(s2, ws)
+print("ALT_OK")
+'''
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=root, **env),
+                       capture_output=True, text=True, timeout=300)
+    assert "ALT_OK" in r.stdout, r.stderr[-3000:]
