@@ -447,6 +447,44 @@ def gpu_arm(args) -> None:
 
     # ---- end to end: host buffers through the C-ABI pipeline (every rank) -------
     e2e = None
+    if not args.no_e2e and cfg["kind"] == "planes":
+        # frames of host planes through adct_pipeline_compress_quant_planes
+        m = min(per, max(1, args.e2e_images // 4))
+        host_in = [pinned_empty((m,) + tuple(p.shape[1:])) for p in planes]
+        host_out = [pinned_empty(a.shape) for a in host_in]
+        for a, p in zip(host_in, planes):
+            a[...] = p[:m].cpu().numpy()
+        qt4 = quant.quant_table(cfg["q"])
+        try:
+            with HostPipeline(local, chunk_bytes=max(args.e2e_chunk_mb << 20, 2 * sum(a[0].nbytes for a in host_in))) as pipe:
+                def timed_planes(outs):
+                    pipe.compress_quant_planes(host_in, qt4, outs, register=False)
+                    if world > 1:
+                        dist.barrier()
+                    t0 = time.perf_counter()
+                    for _ in range(3):
+                        pipe.compress_quant_planes(host_in, qt4, outs, register=False)
+                    dt = (time.perf_counter() - t0) / 3
+                    if world > 1:
+                        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                        dt = t.item()
+                    return dt
+                dt = timed_planes(host_out)
+                dt_metric = timed_planes(None)
+            px = world * sum(a.size for a in host_in)
+            nbytes = sum(a.nbytes for a in host_in)
+            e2e = {"value": px / dt / 1e9, "unit": UNIT,
+                   "h2d_bytes_per_step": int(world * nbytes),
+                   "d2h_bytes_per_step": int(world * (nbytes + 8 * 3 * m)),
+                   "frames_per_step": world * m,
+                   "api": "adct_pipeline_compress_quant_planes (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks",
+                   "metric_only": {"value": px / dt_metric / 1e9, "unit": UNIT,
+                                   "h2d_bytes_per_step": int(world * nbytes),
+                                   "d2h_bytes_per_step": int(world * 8 * 3 * m),
+                                   "note": "reconstructions kept on the device; only the per-frame, per-plane SSE is read back"}}
+        finally:
+            del host_in, host_out
     if not args.no_e2e and cfg["kind"] in ("retain", "quant"):
         m = min(per, args.e2e_images)
         # page-locked host buffers from adct_host_alloc (cudaHostAlloc); the

@@ -258,6 +258,12 @@ int adct_pipeline_compress_retain(adct_pipeline_t* p, const uint8_t* host_img,
 int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img,
                                  uint8_t* host_rec, int64_t n, int32_t h, int32_t w,
                                  const adct_qtab_t* qtab, uint64_t* host_sse);
+/* Frames of 1..3 planes in HOST memory (adct_plane_t with host src/dst;
+ * dst nullable): the quantised pipeline of adct_compress_quant_planes,
+ * streamed in chunks of frames.  host_sse: uint64 [n_frames][n_planes]. */
+int adct_pipeline_compress_quant_planes(adct_pipeline_t* p, const adct_plane_t* host_planes,
+                                        int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
+                                        uint64_t* host_sse);
 /* Page-lock / unlock caller memory (cudaHostRegister). */
 int adct_host_register(void* ptr, size_t bytes);
 int adct_host_unregister(void* ptr);

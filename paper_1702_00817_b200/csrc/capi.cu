@@ -798,6 +798,99 @@ void pipeline_free(adct_pipeline* p) {
   delete p;
 }
 
+// Staging slots of at least `unit_bytes` (one image / one frame of planes)
+// and a device SSE vector of at least `n_sse` entries.
+int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse) {
+  if (unit_bytes > p->chunk_bytes) {  // one unit larger than a chunk: grow the staging buffers
+    for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+    const size_t nb = (unit_bytes + 15) / 16 * 16;
+    for (int k = 0; k < p->depth; ++k) {
+      ADCT_CUDA_TRY(cudaFree(p->d_in[k]));
+      ADCT_CUDA_TRY(cudaFree(p->d_out[k]));
+      p->d_in[k] = p->d_out[k] = nullptr;
+      ADCT_CUDA_TRY(cudaMalloc(&p->d_in[k], nb));
+      ADCT_CUDA_TRY(cudaMalloc(&p->d_out[k], nb));
+    }
+    p->chunk_bytes = nb;
+  }
+  if (n_sse > p->sse_cap) {  // grow the per-call device SSE vector
+    if (p->d_sse) ADCT_CUDA_TRY(cudaFree(p->d_sse));
+    p->d_sse = nullptr;
+    p->sse_cap = 0;
+    ADCT_CUDA_TRY(cudaMalloc(&p->d_sse, (size_t)n_sse * sizeof(uint64_t)));
+    p->sse_cap = n_sse;
+  }
+  return ADCT_OK;
+}
+
+// Frames of 1..3 host planes (e.g. 4:2:0 video): each chunk of frames is
+// gathered plane by plane (one 2-D copy per plane) into a frame-interleaved
+// staging slot [plane 0 | plane 1 | plane 2] per frame, compressed by the
+// one-launch planes kernel, and scattered back the same way.
+int pipeline_planes_run(adct_pipeline* p, const adct_plane_t* hp, int32_t n_planes, int64_t n_frames,
+                        const adct_qtab_t* qtab, uint64_t* host_sse) {
+  if (p == nullptr || hp == nullptr || qtab == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
+    return ADCT_ERR_INVALID_ARGUMENT;
+  size_t off[3] = {0, 0, 0}, frame_bytes = 0;
+  bool any_dst = false;
+  for (int k = 0; k < n_planes; ++k) {
+    const adct_plane_t& q = hp[k];
+    if (q.height < 0 || q.width < 0 || (q.height % 8) || (q.width % 8)) return ADCT_ERR_BAD_DIMENSIONS;
+    const int64_t px = (int64_t)q.height * q.width;
+    if (n_frames > 0 && px > 0 && q.src == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+    if (n_frames > 1 && (q.src_frame_stride < px || (q.dst && q.dst_frame_stride < px)))
+      return ADCT_ERR_INVALID_ARGUMENT;
+    off[k] = frame_bytes;
+    frame_bytes += ((size_t)px + 15) / 16 * 16;
+    any_dst = any_dst || q.dst != nullptr;
+  }
+  if (n_frames == 0) return ADCT_OK;
+  if (host_sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (frame_bytes == 0) {
+    std::memset(host_sse, 0, (size_t)n_frames * n_planes * sizeof(uint64_t));
+    return ADCT_OK;
+  }
+  ADCT_CUDA_TRY(cudaSetDevice(p->device));
+  int rc0 = pipeline_reserve(p, frame_bytes, n_frames * n_planes);
+  if (rc0 != ADCT_OK) return rc0;
+  const int64_t per = (int64_t)(p->chunk_bytes / frame_bytes);
+  int64_t chunk = 0;
+  for (int64_t f0 = 0; f0 < n_frames; f0 += per, ++chunk) {
+    const int b = (int)(chunk % p->depth);
+    const int64_t m = (n_frames - f0) < per ? (n_frames - f0) : per;
+    cudaStream_t s = p->stream[b];
+    adct_plane_t dev[3];
+    for (int k = 0; k < n_planes; ++k) {
+      const adct_plane_t& q = hp[k];
+      const size_t row = (size_t)q.height * q.width;
+      const size_t sfs = m > 1 ? (size_t)q.src_frame_stride : row;
+      if (row)
+        ADCT_CUDA_TRY(cudaMemcpy2DAsync(p->d_in[b] + off[k], frame_bytes, q.src + f0 * q.src_frame_stride, sfs,
+                                        row, (size_t)m, cudaMemcpyHostToDevice, s));
+      dev[k].src = p->d_in[b] + off[k];
+      dev[k].dst = any_dst ? p->d_out[b] + off[k] : nullptr;
+      dev[k].height = q.height;
+      dev[k].width = q.width;
+      dev[k].src_frame_stride = (int64_t)frame_bytes;
+      dev[k].dst_frame_stride = (int64_t)frame_bytes;
+    }
+    int rc = adct_compress_quant_planes(dev, n_planes, m, qtab, p->d_sse + f0 * n_planes, s);
+    if (rc != ADCT_OK) return rc;
+    for (int k = 0; k < n_planes; ++k) {
+      const adct_plane_t& q = hp[k];
+      const size_t row = (size_t)q.height * q.width;
+      if (q.dst == nullptr || row == 0) continue;
+      const size_t dfs = m > 1 ? (size_t)q.dst_frame_stride : row;
+      ADCT_CUDA_TRY(cudaMemcpy2DAsync(q.dst + f0 * q.dst_frame_stride, dfs, p->d_out[b] + off[k], frame_bytes,
+                                      row, (size_t)m, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+  ADCT_CUDA_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n_frames * n_planes * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost));
+  return ADCT_OK;
+}
+
 // kind: 0 retain (r), 1 quant (qtab)
 int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, int64_t n, int32_t h,
                  int32_t w, int kind, int32_t r, const adct_qtab_t* qtab, uint64_t* host_sse) {
@@ -813,26 +906,9 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
     return ADCT_OK;
   }
   ADCT_CUDA_TRY(cudaSetDevice(p->device));
-  if ((size_t)px > p->chunk_bytes) {  // one image larger than a chunk: grow the staging buffers
-    for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
-    const size_t nb = ((size_t)px + 15) / 16 * 16;
-    for (int k = 0; k < p->depth; ++k) {
-      ADCT_CUDA_TRY(cudaFree(p->d_in[k]));
-      ADCT_CUDA_TRY(cudaFree(p->d_out[k]));
-      p->d_in[k] = p->d_out[k] = nullptr;
-      ADCT_CUDA_TRY(cudaMalloc(&p->d_in[k], nb));
-      ADCT_CUDA_TRY(cudaMalloc(&p->d_out[k], nb));
-    }
-    p->chunk_bytes = nb;
-  }
+  int rc0 = pipeline_reserve(p, (size_t)px, n);
+  if (rc0 != ADCT_OK) return rc0;
   const int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
-  if (n > p->sse_cap) {  // grow the per-call device SSE vector
-    if (p->d_sse) ADCT_CUDA_TRY(cudaFree(p->d_sse));
-    p->d_sse = nullptr;
-    p->sse_cap = 0;
-    ADCT_CUDA_TRY(cudaMalloc(&p->d_sse, (size_t)n * sizeof(uint64_t)));
-    p->sse_cap = n;
-  }
   // Chunk i goes to stream i % 3: its H2D, kernel and D2H are ordered on that
   // stream, and the copy engines overlap chunk i's D2H with chunk i+1's H2D.
   // Nothing in the loop blocks the host (no pageable-memory copies).
@@ -903,6 +979,12 @@ int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img, ui
                                  int64_t n, int32_t h, int32_t w, const adct_qtab_t* qtab,
                                  uint64_t* host_sse) {
   return pipeline_run(p, host_img, host_rec, n, h, w, 1, 0, qtab, host_sse);
+}
+
+int adct_pipeline_compress_quant_planes(adct_pipeline_t* p, const adct_plane_t* host_planes,
+                                        int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
+                                        uint64_t* host_sse) {
+  return pipeline_planes_run(p, host_planes, n_planes, n_frames, qtab, host_sse);
 }
 
 int adct_host_register(void* ptr, size_t bytes) {

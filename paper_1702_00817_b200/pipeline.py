@@ -72,6 +72,41 @@ class HostPipeline:
         return rec, sse.astype(np.int64)
 
 
+    def compress_quant_planes(self, planes, qtab, outs=None, *, register: bool = True):
+        """Frames of 1..3 host planes (each (N, H_k, W_k) uint8, e.g. Y/Cb/Cr of
+        4:2:0 video) through the one-launch planes kernel in chunks of frames.
+        `outs`: matching arrays for the reconstructions, or None (SSE only).
+        Returns (outs, sse int64 [N, n_planes])."""
+        from ._lib import Plane
+
+        planes = list(planes)
+        if not 1 <= len(planes) <= 3:
+            raise ValueError("1 to 3 planes")
+        n = planes[0].shape[0]
+        for k, a in enumerate(planes):
+            self._check(a)
+            if a.shape[0] != n:
+                raise ValueError(f"plane {k} has {a.shape[0]} frames, plane 0 has {n}")
+        if outs is not None:
+            outs = list(outs)
+            if len(outs) != len(planes) or any(o.shape != a.shape or o.dtype != np.uint8 or not o.flags.c_contiguous
+                                               for o, a in zip(outs, planes)):
+                raise ValueError("outs must match the planes' shapes (C-contiguous uint8)")
+        arr = (Plane * len(planes))()
+        for k, a in enumerate(planes):
+            h, w = a.shape[1], a.shape[2]
+            arr[k].src = a.ctypes.data
+            arr[k].dst = outs[k].ctypes.data if outs is not None else None
+            arr[k].height, arr[k].width = h, w
+            arr[k].src_frame_stride = h * w
+            arr[k].dst_frame_stride = h * w
+        sse = np.zeros((n, len(planes)), dtype=np.uint64)
+        with _Pinned(planes + (outs or []) if register else []):
+            _lib.call("adct_pipeline_compress_quant_planes", self._h, ctypes.addressof(arr), len(planes), n,
+                      ctypes.byref(qtab), sse.ctypes.data)
+        return outs, sse.astype(np.int64)
+
+
 class _Pinned:
     """Page-lock numpy buffers for the duration of a call."""
 

@@ -137,6 +137,28 @@ def test_host_pipeline_retain_and_quant(cuda, chunk_mb):
         assert np.array_equal(sse_small, exact.compress_retain(imgs, 10)[1])
 
 
+@pytest.mark.parametrize("chunk", [1 << 14, 1 << 22])
+def test_host_pipeline_planes(cuda, chunk):
+    """adct_pipeline_compress_quant_planes: host Y/Cb/Cr frames, chunked by
+    frames (small chunk: one frame per chunk, staging grows), with and without
+    reconstructions, against the per-plane oracle."""
+    rng = np.random.default_rng(9)
+    y = rng.integers(0, 256, (5, 48, 64), dtype=np.uint8)
+    cb = rng.integers(0, 256, (5, 24, 32), dtype=np.uint8)
+    cr = rng.integers(0, 256, (5, 24, 32), dtype=np.uint8)
+    for q in (10, 75):
+        qt = quant.quant_table(q)
+        outs = [np.empty_like(p) for p in (y, cb, cr)]
+        with HostPipeline(0, chunk_bytes=chunk) as p:
+            got, sse = p.compress_quant_planes([y, cb, cr], qt, outs)
+            _, sse_only = p.compress_quant_planes([y, cb, cr], qt)
+        qp = quant.qtab_qprime(qt)
+        for k, plane in enumerate((y, cb, cr)):
+            wr, ws = exact.compress_quant(plane, qp)
+            assert np.array_equal(got[k], wr) and np.array_equal(sse[:, k], ws), (q, k)
+            assert np.array_equal(sse_only[:, k], ws)
+
+
 def test_pinned_empty_buffers_through_pipeline(cuda):
     import gc
 
