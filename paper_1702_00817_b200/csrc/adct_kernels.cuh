@@ -1,5 +1,19 @@
 // adct_kernels.cuh — sm_100a kernels of the approximate-DCT hot path.
 // See adct_device.cuh for the arithmetic model and DESIGN.md for rooflines.
+//
+//   K2  k_retain<R,PAIR>      compress_image + mse, r pruned at compile time
+//                             (reference codec.py:144-155, metrics.py:49-56)
+//   K2' k_retain_rt<PAIR,F>   same, runtime r; optional unrounded SSE
+//   K3  k_quant_p / k_quant   quantised pipeline, two blocks per thread
+//                             (forward_2d_unscaled + folded Q' + inverse_2d,
+//                             codec.py:74-104)
+//   K3" k_quant_hybrid        coarse tables: packed forward/quantiser, 32-bit inverse
+//   K3' k_quant_wide          remaining coarse tables, one block per thread
+//   K7  k_sweep_inc / k_sweep SSE for every r from one read (cli.py:101-113)
+//   K1  k_forward<PAIR,T>     T X T^T coefficients in _tile order (codec.py:74-81,107-131)
+//   f64 / dense kernels       real-valued and non-proposed transforms (codec.py:68-71,84-87;
+//                             kernels.py:166-178)
+//   k_synth                   BASELINE's blob generator (input only, never timed)
 #pragma once
 
 #include "adct_device.cuh"
