@@ -79,3 +79,33 @@ def test_forward_and_sweep_write_only_their_outputs(cuda, n, h, w, gap):
     torch.cuda.synchronize()
     assert s.shape == (n, 7)
     assert np.array_equal(s.cpu().numpy(), exact.sweep_sse(x.numpy(), 3, 9))
+
+
+@pytest.mark.parametrize("h,w", [(8, 65536), (65536, 16), (8, 8), (16384, 16384)])
+def test_extreme_geometries(cuda, h, w):
+    """Row-index arithmetic at the extremes: one block row of 4096 units,
+    one unit per block row (upr == 1), a single block, and a 256 MiB image.
+    Full oracle comparison where it is cheap, sampled otherwise."""
+    g = torch.Generator().manual_seed(h + w)
+    x = torch.randint(0, 256, (1, h, w), dtype=torch.uint8, generator=g).to(cuda)
+    rec, sse, _ = batch.compress_retain(x, 10)
+    qt = quant.quant_table(50)
+    recq, sseq = batch.compress_quant(x, qt)
+    torch.cuda.synchronize()
+    if h * w <= (1 << 20):
+        host = x.cpu().numpy()
+        wr, ws, _ = exact.compress_retain(host, 10)
+        assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws)
+        wq, wqs = exact.compress_quant(host, quant.qtab_qprime(qt))
+        assert np.array_equal(recq.cpu().numpy(), wq) and np.array_equal(sseq.cpu().numpy(), wqs)
+    else:  # 8-row bands at the start, middle and end: blocks are independent
+        for r0 in (0, h // 2, h - 64):
+            band = x[:, r0:r0 + 64].contiguous().cpu().numpy()
+            wr, _, _ = exact.compress_retain(band, 10)
+            assert np.array_equal(rec[:, r0:r0 + 64].cpu().numpy(), wr), r0
+            wq, _ = exact.compress_quant(band, quant.qtab_qprime(qt))
+            assert np.array_equal(recq[:, r0:r0 + 64].cpu().numpy(), wq), r0
+        d = rec.to(torch.int64) - x.to(torch.int64)
+        assert int(sse[0]) == int((d * d).sum())
+        dq = recq.to(torch.int64) - x.to(torch.int64)
+        assert int(sseq[0]) == int((dq * dq).sum())
