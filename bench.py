@@ -6,9 +6,13 @@
 
 A step = one fused compress launch over every image resident on the rank
 (config 3: 4096 seeded 2048x2048 uint8 images per GPU, retain r=10; weak
-scaling) + the NCCL all-reduce of the per-image SSE when N > 1.  Inputs are
-generated on the GPU before timing (16 GiB per GPU >> 126 MB L2, so no L2
-flush is needed between steps).  Rank 0 prints one JSON line.
+scaling) + the NCCL all-reduce of the per-image SSE when N > 1 (or, with
+--exchange fused, the exchange done by the kernel epilogue through torch
+symmetric memory).  Inputs are generated on the GPU before timing (16 GiB per
+GPU >> 126 MB L2, so no L2 flush is needed between steps).  `e2e` times the
+same work through the C-ABI host pipeline from page-locked host buffers
+(reconstructions returned; `e2e.metric_only`: only the SSE/PSNR vector).
+Rank 0 prints one JSON line.
 
 --impl reference times the reference's own CPU algorithm (the float64
 restatement oracle/refport.py of codec.compress_image + metrics.mse/psnr;
@@ -41,7 +45,7 @@ CONFIGS = {
     4: dict(kind="planes", frames=512, q=75,
             workload="config4: 512 seeded 3840x2160 YCbCr 4:2:0 frames per GPU, fused quant(q=75) of Y+Cb+Cr in one launch"),
     1: dict(kind="sweep", h=512, w=512, n=45, r=(1, 45), blobs=(16, 8.0, 64.0),
-            workload="config1: 45 seeded 512x512 u8 images, SSE/PSNR for every r=1..45 from one read (k_sweep); "
+            workload="config1: 45 seeded 512x512 u8 images, SSE/PSNR for every r=1..45 from one read (k_sweep_inc); "
                      "11.8 MB, L2-resident and launch bound: value counts image pixels, not pixel-reconstructions"),
     0: dict(kind="forward", h=512, w=512, n=1, blobs=(16, 8.0, 64.0),
             workload="config0: 1 seeded 512x512 u8 image, exact int32 T X T^T coefficients (launch bound)"),
