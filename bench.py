@@ -372,17 +372,26 @@ def gpu_arm(args) -> None:
         recs = [torch.empty_like(p) for p in planes]
         arr, _ = batch._planes(planes, recs)
         sse = torch.empty((frames, 3), dtype=torch.int64, device=dev)
-        def step_kernel():
-            _lib.call("adct_compress_quant_planes", arr, 3, frames, ctypes.byref(qt), sse.data_ptr(),
-                      torch.cuda.current_stream().cuda_stream)
+        n_total = frames * world if args.scaling == "weak" else cfg["frames"]
+        if args.exchange == "fused":  # exchange of the (frame, plane) SSE in the kernel epilogue
+            if not dist.is_initialized():
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29562")
+                dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+            exchange = shard.SseExchange(n_total * 3, dev)
+            def step_kernel():
+                exchange.compress_quant_planes(planes, qt, f0, out=recs)
+        else:
+            def step_kernel():
+                _lib.call("adct_compress_quant_planes", arr, 3, frames, ctypes.byref(qt), sse.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
         launches_per_step = 1
         px_rank = frames * sum(p.shape[1] * p.shape[2] for p in planes)
-        n_total = frames * world if args.scaling == "weak" else cfg["frames"]
         per = frames
     torch.cuda.synchronize()
     log(f"[rank {rank}] workload ready in {time.perf_counter() - t_gen:.1f}s: {px_rank / 1e9:.2f} Gpx per step")
 
-    fused_exchange = cfg["kind"] == "retain" and args.exchange == "fused"
+    fused_exchange = cfg["kind"] in ("retain", "planes") and args.exchange == "fused"
 
     def step():
         step_kernel()
@@ -594,7 +603,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="configs 0/1: launch through the C ABI every step")
     ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "fused"],
-                    help="retain configs: SSE exchange by NCCL all-reduce (default) or fused into the kernel "
+                    help="configs 3 and 4: SSE exchange by NCCL all-reduce (default) or fused into the kernel "
                          "epilogue through torch symmetric memory")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

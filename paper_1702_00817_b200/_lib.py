@@ -76,6 +76,10 @@ PROTOTYPES = {
         [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int64, c_int64, c_int32, c_void_p, c_void_p,
          c_int32, c_int64, c_void_p, c_void_p],
     ),
+    "adct_compress_quant_planes_exchange": (
+        c_int,
+        [c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p],
+    ),
     "adct_compress_quant": (
         c_int,
         [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int64, c_int64, POINTER(QTab), c_void_p, c_void_p],

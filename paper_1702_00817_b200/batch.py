@@ -193,6 +193,23 @@ def compress_quant_planes(planes: Sequence[torch.Tensor], qtab: _lib.QTab, *, re
     return recs, sse
 
 
+def compress_quant_planes_exchange(planes: Sequence[torch.Tensor], qtab: _lib.QTab, peers_dev: int, n_peers: int,
+                                   peer_offset: int, arrivals: torch.Tensor, *, reconstruct: bool = True,
+                                   out: Sequence[torch.Tensor] | None = None):
+    """compress_quant_planes whose epilogue also stores each (frame, plane)'s
+    exact SSE into every peer's vector at peer_offset + frame * n_planes +
+    plane (see compress_retain_exchange).  `arrivals`: zeroed int32
+    [N * n_planes] scratch, left zeroed.  Returns (recs, local sse (N, n_planes))."""
+    recs = list(out) if out is not None else [torch.empty_like(p) if reconstruct else None for p in planes]
+    arr, n = _planes(planes, recs)
+    if arrivals.dtype != torch.int32 or arrivals.numel() < n * len(planes) or arrivals.device != planes[0].device:
+        raise ValueError("arrivals must be an int32 tensor of >= N * n_planes zeros on the planes' device")
+    sse = torch.empty((n, len(planes)), dtype=torch.int64, device=planes[0].device)
+    _lib.call("adct_compress_quant_planes_exchange", arr, len(planes), n, ctypes.byref(qtab), _ptr(sse),
+              int(peers_dev), int(n_peers), int(peer_offset), _ptr(arrivals), _stream())
+    return recs, sse
+
+
 def compress_retain_planes(planes: Sequence[torch.Tensor], r: int, *, reconstruct: bool = True):
     if not 1 <= int(r) <= 64:
         raise InvalidRetention(f"retention count must be in [1, 64], got {r}")

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kRetainThreads) k_retain(PlaneSetDev ps, u64* 
     inv2d(W, U);
     acc = emit_unit<PAIR>(U, w, L.dst, L.width);
   }
-  if (sse != nullptr) cta_sum_add<kRetainThreads>(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x);
+  if (sse != nullptr)
+    cta_sum_add<kRetainThreads>(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
 }
 
 // Runtime-r variant: ragged widths (PAIR=false) and the exact "unrounded"
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
   }
-  if (sse != nullptr) cta_sum_add(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x);
+  if (sse != nullptr) cta_sum_add(cta, acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
   if (FSSE) block_add_u64(accf, ssef + L.frame * ps.n_planes + L.plane);
 }
 
@@ -176,7 +177,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   // Per-warp atomics: measured 8% faster than the per-CTA accumulator for
   // this issue-bound kernel (the memory-bound retain kernels prefer per-CTA).
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr)
+    warp_sse_add<kThreads>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
 }
 
 // ---------------------------------------------------------------------------
@@ -243,7 +245,7 @@ __device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <bool PAIR, bool FLIP>
+template <bool PAIR, bool FLIP, bool XCHG = false>
 __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
@@ -301,7 +303,12 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
       }
       acc = emit_unit<PAIR, FLIP>(U, wo, cur.dst, cur.width);
     }
-    if (sse != nullptr) block_add_u32(acc, sse + cur.frame * ps.n_planes + cur.plane);
+    if (sse != nullptr) {
+      if (XCHG)
+        warp_sse_add<kThreads, true>(acc, sse, cur.frame * ps.n_planes + cur.plane, ps.x, ps.p[cur.plane].units);
+      else
+        block_add_u32(acc, sse + cur.frame * ps.n_planes + cur.plane);
+    }
     cur = nxt;
     if (nt >= n_tiles) break;
   }
@@ -584,6 +591,7 @@ __device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
 
 constexpr size_t kHybridSmem = (size_t)64 * kThreads * sizeof(int) + (size_t)8 * kThreads * sizeof(uint4);
 
+template <bool XCHG>
 __global__ void __launch_bounds__(kThreads, 2)
     k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
   extern __shared__ uint4 s_dyn[];
@@ -660,7 +668,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       acc = sse4(wi.w, o.y, acc);
     }
   }
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr)
+    warp_sse_add<kThreads, XCHG>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
 }
 
 // K3 for coarse tables (wide == 1, e.g. q < 25): one block per thread.  The
@@ -717,7 +726,8 @@ __global__ void __launch_bounds__(kThreads)
       acc = sse4(w[i].y, hi, acc);
     }
   }
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+  if (sse != nullptr)
+    warp_sse_add<kThreads>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
 }
 
 // ---------------------------------------------------------------------------

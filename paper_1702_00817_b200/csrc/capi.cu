@@ -421,10 +421,7 @@ static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n
   PlaneSetHost ps;
   int rc = build_planes(planes, n_planes, n_frames, ps);
   if (rc != ADCT_OK) return rc;
-  if (xchg != nullptr) {  // single plane, no unrounded SSE (checked by the caller)
-    ps.dev.x = *xchg;
-    ps.dev.x.ctas_per_image = (uint32_t)ps.grid_x;
-  }
+  if (xchg != nullptr) ps.dev.x = *xchg;  // no unrounded SSE with an exchange (checked by the caller)
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
@@ -435,10 +432,7 @@ static int retain_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n
     PlaneSetHost ps128;  // the pruned retain kernels run 128-unit tiles
     rc = build_planes(planes, n_planes, n_frames, ps128, false, kRetainThreads);
     if (rc != ADCT_OK) return rc;
-    if (xchg != nullptr) {
-      ps128.dev.x = *xchg;
-      ps128.dev.x.ctas_per_image = (uint32_t)ps128.grid_x;
-    }
+    if (xchg != nullptr) ps128.dev.x = *xchg;
     RetainKernel k = retain_kernel(r);
     return for_frame_chunks(ps128, n_frames, [&](dim3 g) { k<<<g, kRetainThreads, 0, s>>>(ps128.dev, d_sse); });
   }
@@ -475,7 +469,7 @@ int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, i
   x.arrivals = arrivals;
   x.offset = peer_offset;
   x.n_peers = n_peers;
-  x.ctas_per_image = 0;  // set from the launch geometry
+  x.packed = 0;  // retain kernels count CTAs with a fence (one per CTA, memory-bound kernel)
   adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
   return retain_planes(&pl, 1, n, r, sse, nullptr, stream, &x);
 }
@@ -486,8 +480,38 @@ int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes, in
 }
 
 // --- K3/K6 quant -------------------------------------------------------------
+static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
+                        uint64_t* sse, void* stream, const XchgDev* xchg);
+
 int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,
                                const adct_qtab_t* qtab, uint64_t* sse, void* stream) {
+  return quant_planes(planes, n_planes, n_frames, qtab, sse, stream, nullptr);
+}
+
+int adct_compress_quant_planes_exchange(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,
+                                        const adct_qtab_t* qtab, uint64_t* sse, uint64_t* const* peer_sse,
+                                        int32_t n_peers, int64_t peer_offset, uint32_t* arrivals,
+                                        void* stream) {
+  if (n_frames < 0 || n_peers < 1 || n_peers > 1024 || peer_offset < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (n_frames == 0) return quant_planes(planes, n_planes, 0, qtab, sse, stream, nullptr);
+  if (sse == nullptr || peer_sse == nullptr || arrivals == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (!aligned(sse, 8) || !aligned(peer_sse, 8) || !aligned(arrivals, 4)) return ADCT_ERR_MISALIGNED;
+  XchgDev x;
+  x.peers = reinterpret_cast<u64* const*>(peer_sse);
+  x.arrivals = arrivals;
+  x.offset = peer_offset;
+  x.n_peers = n_peers;
+  // packed arrival counting needs < 2^16 warps (256-unit tiles) per plane
+  x.packed = 1;
+  for (int k = 0; planes != nullptr && k < n_planes && k < 3; ++k) {
+    const int64_t units = (int64_t)planes[k].height / 8 * (planes[k].width / 8);  // upper bound (single-block units)
+    if ((units + 255) / 256 * 8 > 65535) x.packed = 0;
+  }
+  return quant_planes(planes, n_planes, n_frames, qtab, sse, stream, &x);
+}
+
+static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
+                        uint64_t* sse, void* stream, const XchgDev* xchg) {
   if (qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   for (int p = 0; p < 64; ++p)
     if (qtab->qprime[p] < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
@@ -496,6 +520,7 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
   PlaneSetHost ps;
   int rc = build_planes(planes, n_planes, n_frames, ps, wide);
   if (rc != ADCT_OK) return rc;
+  if (xchg != nullptr) ps.dev.x = *xchg;
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
@@ -506,11 +531,12 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
       PlaneSetHost ph;  // two blocks per thread where every plane pairs
       rc = build_planes(planes, n_planes, n_frames, ph, false);
       if (rc != ADCT_OK) return rc;
+      if (xchg != nullptr) ph.dev.x = *xchg;
       if (ph.pair) {
-        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kHybridSmem));
+        auto kh = xchg != nullptr ? k_quant_hybrid<true> : k_quant_hybrid<false>;
+        ADCT_CUDA_TRY(cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHybridSmem));
         return for_frame_chunks(ph, n_frames, [&](dim3 g) {
-          k_quant_hybrid<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
+          kh<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
         });
       }
     }
@@ -527,11 +553,17 @@ int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int
     if ((int64_t)grid > n_tiles) grid = (int)n_tiles;
     ps.dev.frame_base = 0;
     const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
-#define ADCT_QP(PA, FL)                                                                        \
-  do {                                                                                         \
-    ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL>,                                      \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_quant_p<PA, FL><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x);      \
+#define ADCT_QP(PA, FL)                                                                          \
+  do {                                                                                           \
+    if (xchg != nullptr) {                                                                       \
+      ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL, true>,                                \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      k_quant_p<PA, FL, true><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x); \
+    } else {                                                                                     \
+      ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL, false>,                               \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      k_quant_p<PA, FL, false><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x); \
+    }                                                                                            \
   } while (0)
     if (ps.pair) {
       if (al) ADCT_QP(true, false); else ADCT_QP(true, true);

@@ -139,3 +139,20 @@ class SseExchange:
         self._hdl.barrier(channel=0)  # stream-ordered: every rank's pushes are visible after this
         return rec, local
 
+    def compress_quant_planes(self, planes, qtab, frame_offset: int, *, out=None):
+        """Frames [frame_offset, frame_offset + N) of n_planes planes; the
+        vector holds entry frame * n_planes + plane (n_total = frames * planes)."""
+        from . import batch
+
+        n, k = planes[0].shape[0], len(planes)
+        off = int(frame_offset) * k
+        if frame_offset < 0 or off + n * k > self.n_total:
+            raise ValueError(f"frames [{frame_offset}, {frame_offset + n}) x {k} planes outside the exchange vector")
+        if self._arrivals is None or self._arrivals.numel() < n * k:
+            self._arrivals = torch.zeros(max(n * k, 1), dtype=torch.int32, device=planes[0].device)
+        recs, local = batch.compress_quant_planes_exchange(
+            planes, qtab, self._hdl.buffer_ptrs_dev, self.n_peers, off, self._arrivals, out=out
+        )
+        self._hdl.barrier(channel=0)
+        return recs, local
+

@@ -77,8 +77,45 @@ for rep in range(2):
     torch.cuda.synchronize()
     assert torch.equal(ex.sse[:9], want), (ex.sse, want)
     assert int(ex.sse[9:].abs().sum()) == 0
+from paper_1702_00817_b200 import quant
+planes = [x[:, :128, :].contiguous(), x[:, :64, :128].contiguous(), x[:, 64:128, 128:].contiguous()]
+qt = quant.quant_table(75)
+_, wantq = batch.compress_quant_planes(planes, qt)
+exq = shard.SseExchange(9 * 3 + 3, "cuda")
+exq.compress_quant_planes([p[:4] for p in planes], qt, 0)
+exq.compress_quant_planes([p[4:] for p in planes], qt, 4)
+torch.cuda.synchronize()
+assert torch.equal(exq.sse[:27], wantq.reshape(-1)), (exq.sse, wantq)
 dist.destroy_process_group()
 print("EXCHANGE_OK")
 '''
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert "EXCHANGE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("cr_w", [48, 40])
+@pytest.mark.parametrize("q", [75, 30, 10, 2])
+def test_quant_planes_exchange_on_local_peers(cuda, q, cr_w):
+    """Quant kernels with the fused exchange (persistent packed q >= 25,
+    hybrid q = 10, scalar q = 2) over three planes; a 40-px plane makes the
+    whole launch single-block (unpaired)."""
+    from paper_1702_00817_b200 import quant
+
+    g = torch.Generator().manual_seed(q)
+    y = torch.randint(0, 256, (4, 48, 96), dtype=torch.uint8, generator=g).to(cuda)
+    cb = torch.randint(0, 256, (4, 24, 48), dtype=torch.uint8, generator=g).to(cuda)
+    cr = torch.randint(0, 256, (4, 24, cr_w), dtype=torch.uint8, generator=g).to(cuda)
+    qt = quant.quant_table(q)
+    recs_ref, sse_ref = batch.compress_quant_planes([y, cb, cr], qt)
+    offset, total = 6, 4 * 3 + 9
+    peers = [torch.full((total,), -5, dtype=torch.int64, device=cuda) for _ in range(2)]
+    ptrs = _peer_array(peers)
+    arrivals = torch.zeros(12, dtype=torch.int32, device=cuda)
+    for rep in range(2):
+        recs, local = batch.compress_quant_planes_exchange([y, cb, cr], qt, ptrs.data_ptr(), 2, offset, arrivals)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, b) for a, b in zip(recs, recs_ref)) and torch.equal(local, sse_ref)
+        for v in peers:
+            assert torch.equal(v[offset:offset + 12], sse_ref.reshape(-1))
+            assert bool((v[:offset] == -5).all()) and bool((v[offset + 12:] == -5).all())
+        assert int(arrivals.abs().sum()) == 0
