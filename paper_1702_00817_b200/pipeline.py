@@ -17,7 +17,9 @@ from .errors import BadDimensions, InvalidRetention
 
 
 class HostPipeline:
-    def __init__(self, device: int = 0, chunk_bytes: int = 256 << 20):
+    def __init__(self, device: int = 0, chunk_bytes: int = 32 << 20):
+        # 32-64 MiB chunks measured fastest (tools/e2e_sweep.py): larger ones
+        # lengthen the pipeline's fill and drain, smaller ones add per-copy gaps
         h = ctypes.c_void_p()
         _lib.call("adct_pipeline_create", int(device), int(chunk_bytes), ctypes.byref(h))
         self._h = h
