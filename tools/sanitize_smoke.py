@@ -28,5 +28,17 @@ synth.images_device([0, 1], 64, 96, 16, 8.0, 64.0, device=dev)
 imgs = x.cpu().numpy(); rec = np.empty_like(imgs)
 with HostPipeline(0, chunk_bytes=64 * 96 * 2) as p:
     p.compress_retain(imgs, 10, rec); p.compress_quant(imgs, quant.quant_table(50), rec)
+    hp = [pl.cpu().numpy() for pl in planes]
+    p.compress_quant_planes(hp, quant.quant_table(10), [np.empty_like(a) for a in hp])
+from paper_1702_00817_b200.pipeline import pinned_empty
+buf = pinned_empty((2, 64, 96)); buf[...] = 7
+batch.compress_quant(x, quant.quant_table(2))  # Q' > 8191 somewhere: scalar coarse-table kernel
+peers = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(2)]
+ptrs = torch.tensor([v.data_ptr() for v in peers], dtype=torch.int64, device=dev)
+arr = torch.zeros(9, dtype=torch.int32, device=dev)
+batch.compress_retain_exchange(x, 10, ptrs.data_ptr(), 2, 1, arr)
+peers9 = [torch.zeros(12, dtype=torch.int64, device=dev) for _ in range(2)]
+ptrs9 = torch.tensor([v.data_ptr() for v in peers9], dtype=torch.int64, device=dev)
+batch.compress_quant_planes_exchange(planes, quant.quant_table(75), ptrs9.data_ptr(), 2, 1, arr)
 torch.cuda.synchronize()
 print("sanitize smoke done")
