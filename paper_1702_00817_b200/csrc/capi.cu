@@ -836,10 +836,13 @@ int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse) {
   if (unit_bytes > p->chunk_bytes) {  // one unit larger than a chunk: grow the staging buffers
     for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
     const size_t nb = (unit_bytes + 15) / 16 * 16;
+    p->chunk_bytes = 0;  // invalid until every slot is reallocated (a failed grow retries next call)
     for (int k = 0; k < p->depth; ++k) {
       ADCT_CUDA_TRY(cudaFree(p->d_in[k]));
       ADCT_CUDA_TRY(cudaFree(p->d_out[k]));
       p->d_in[k] = p->d_out[k] = nullptr;
+    }
+    for (int k = 0; k < p->depth; ++k) {
       ADCT_CUDA_TRY(cudaMalloc(&p->d_in[k], nb));
       ADCT_CUDA_TRY(cudaMalloc(&p->d_out[k], nb));
     }
