@@ -394,6 +394,17 @@ __device__ __forceinline__ void cta_sum_add(CtaSum& s, u32 v, u64* sse, int64_t 
     const u64 old = atomicAdd(&s.word, (1ull << 32) | (u64)v);
     if ((u32)(old >> 32) == NT / 32 - 1) {
       const u64 total = (u64)(u32)old + v;
+      if (x.peers != nullptr && x.packed) {  // CTA count in bits 48..63 of the SSE word: one atomic
+        const uint32_t ctas = (plane_units + NT - 1) / NT;
+        const u64 prev = atomicAdd(sse + idx, (1ull << 48) | total);
+        if ((u32)(prev >> 48) == ctas - 1) {
+          const u64 image_sse = (prev & ((1ull << 48) - 1)) + total;
+          sse[idx] = image_sse;
+          for (int p = 0; p < x.n_peers; ++p) x.peers[p][x.offset + idx] = image_sse;
+          __threadfence_system();
+        }
+        return;
+      }
       if (total != 0) atomicAdd(sse + idx, total);
       if (x.peers != nullptr) {
         __threadfence();

@@ -469,7 +469,8 @@ int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, i
   x.arrivals = arrivals;
   x.offset = peer_offset;
   x.n_peers = n_peers;
-  x.packed = 0;  // retain kernels count CTAs with a fence (one per CTA, memory-bound kernel)
+  // packed CTA counting needs < 2^16 CTAs (128- or 256-unit tiles) per image
+  x.packed = ((int64_t)h / 8 * (w / 8) + 127) / 128 <= 65535 ? 1 : 0;
   adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
   return retain_planes(&pl, 1, n, r, sse, nullptr, stream, &x);
 }
