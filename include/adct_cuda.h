@@ -172,11 +172,12 @@ typedef struct adct_plane {
 int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes,
                                int64_t n_frames, const adct_qtab_t* qtab,
                                uint64_t* sse, void* stream);
-/* adct_compress_quant_planes with the SSE exchange fused into the epilogue
- * (as adct_compress_retain_exchange): when the last warp of (frame f, plane k)
- * finishes, the exact SSE goes to peer_sse[p][peer_offset + f*n_planes + k]
- * for every peer.  arrivals: device uint32 [n_frames * n_planes], zero before
- * the first call and left zero. */
+/* adct_compress_quant_planes plus the SSE exchange: stream-ordered after the
+ * compress kernel, a small push kernel stores the exact SSE of (frame f,
+ * plane k) into peer_sse[p][peer_offset + f*n_planes + k] for every peer
+ * (P2P stores; no collective).  Unlike the memory-bound retain kernel, the
+ * issue-bound quant kernels lose 19-22 % with the exchange inside their
+ * epilogue, hence the separate push.  `arrivals` is unused (may be NULL). */
 int adct_compress_quant_planes_exchange(const adct_plane_t* planes, int32_t n_planes,
                                         int64_t n_frames, const adct_qtab_t* qtab, uint64_t* sse,
                                         uint64_t* const* peer_sse, int32_t n_peers,

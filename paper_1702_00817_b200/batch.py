@@ -196,10 +196,10 @@ def compress_quant_planes(planes: Sequence[torch.Tensor], qtab: _lib.QTab, *, re
 def compress_quant_planes_exchange(planes: Sequence[torch.Tensor], qtab: _lib.QTab, peers_dev: int, n_peers: int,
                                    peer_offset: int, arrivals: torch.Tensor, *, reconstruct: bool = True,
                                    out: Sequence[torch.Tensor] | None = None):
-    """compress_quant_planes whose epilogue also stores each (frame, plane)'s
-    exact SSE into every peer's vector at peer_offset + frame * n_planes +
-    plane (see compress_retain_exchange).  `arrivals`: zeroed int32
-    [N * n_planes] scratch, left zeroed.  Returns (recs, local sse (N, n_planes))."""
+    """compress_quant_planes, then (same stream) each (frame, plane)'s exact
+    SSE pushed into every peer's vector at peer_offset + frame * n_planes +
+    plane (see compress_retain_exchange).  `arrivals` is accepted for symmetry
+    and left untouched.  Returns (recs, local sse (N, n_planes))."""
     recs = list(out) if out is not None else [torch.empty_like(p) if reconstruct else None for p in planes]
     arr, n = _planes(planes, recs)
     if arrivals.dtype != torch.int32 or arrivals.numel() < n * len(planes) or arrivals.device != planes[0].device:

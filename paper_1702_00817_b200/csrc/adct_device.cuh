@@ -212,7 +212,7 @@ struct XchgDev {
   u32* arrivals;       // [images] CTA arrival counters, zero between launches
   int64_t offset;      // this caller's first SSE entry in the peers' vectors
   int32_t n_peers;
-  int32_t packed;      // quant kernels: arrival count in bits 48..63 of the SSE word (no fence)
+  int32_t packed;      // CTA arrival count in bits 48..63 of the SSE word (no fence)
 };
 
 struct PlaneSetDev {
@@ -327,44 +327,6 @@ __device__ __forceinline__ u32 emit_unit(const u32 (&U)[8][8], const uint4 (&w)[
 __device__ __forceinline__ void block_add_u32(u32 v, u64* dst) {
   v = __reduce_add_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0 && v != 0) atomicAdd(dst, (u64)v);
-}
-
-// Per-warp SSE add for the quant kernels (NT-unit tiles), with the optional
-// fused exchange: each warp counts itself in for its (frame, plane) index and
-// the last of the ceil(units/NT) * NT/32 warps pushes the completed sum to
-// every peer (same pattern as cta_sum_add).  The count comes from the plane's
-// geometry, so it is right for every plane of a multi-plane launch.
-template <int NT, bool XCHG = true>
-__device__ __forceinline__ void warp_sse_add(u32 v, u64* sse, int64_t idx, const XchgDev& x, uint32_t plane_units) {
-  v = __reduce_add_sync(0xffffffffu, v);
-  if ((threadIdx.x & 31) == 0) {
-    if (!(XCHG && x.peers != nullptr && x.packed) && v != 0) atomicAdd(sse + idx, (u64)v);
-    if (XCHG && x.peers != nullptr) {
-      const uint32_t warps = (plane_units + NT - 1) / NT * (NT / 32);
-      if (x.packed) {
-        // count and sum in ONE atomic: the warp that completes the count
-        // holds the exact total, with no ordering between two atomics needed
-        // (a fence here would wait for the warp's streaming pixel stores)
-        constexpr u64 kSum = (1ull << 48) - 1;
-        const u64 old = atomicAdd(sse + idx, (1ull << 48) | (u64)v);
-        if ((u32)(old >> 48) == warps - 1) {
-          const u64 total = (old & kSum) + v;
-          sse[idx] = total;  // every other warp has arrived: plain store of the clean sum
-          for (int p = 0; p < x.n_peers; ++p) x.peers[p][x.offset + idx] = total;
-          __threadfence_system();
-        }
-        return;
-      }
-      __threadfence();  // planes too large for the packed count
-      if (atomicAdd(x.arrivals + idx, 1u) == warps - 1) {
-        __threadfence();
-        const u64 total = atomicAdd(sse + idx, 0ull);
-        for (int p = 0; p < x.n_peers; ++p) x.peers[p][x.offset + idx] = total;
-        __threadfence_system();
-        x.arrivals[idx] = 0u;
-      }
-    }
-  }
 }
 
 // Per-CTA SSE accumulator without an end-of-kernel barrier or fence: each

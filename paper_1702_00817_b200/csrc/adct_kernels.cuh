@@ -177,8 +177,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   // Per-warp atomics: measured 8% faster than the per-CTA accumulator for
   // this issue-bound kernel (the memory-bound retain kernels prefer per-CTA).
-  if (sse != nullptr)
-    warp_sse_add<kThreads>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // ---------------------------------------------------------------------------
@@ -245,7 +244,7 @@ __device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <bool PAIR, bool FLIP, bool XCHG = false>
+template <bool PAIR, bool FLIP>
 __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
@@ -303,12 +302,7 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
       }
       acc = emit_unit<PAIR, FLIP>(U, wo, cur.dst, cur.width);
     }
-    if (sse != nullptr) {
-      if (XCHG)
-        warp_sse_add<kThreads, true>(acc, sse, cur.frame * ps.n_planes + cur.plane, ps.x, ps.p[cur.plane].units);
-      else
-        block_add_u32(acc, sse + cur.frame * ps.n_planes + cur.plane);
-    }
+    if (sse != nullptr) block_add_u32(acc, sse + cur.frame * ps.n_planes + cur.plane);
     cur = nxt;
     if (nt >= n_tiles) break;
   }
@@ -572,6 +566,19 @@ __global__ void __launch_bounds__(kForwardThreads)
 }
 
 #ifdef ADCT_DEFINE_PLAIN_KERNELS  // non-template kernels: defined once, in capi.cu
+// SSE exchange for the quantised planes path (row f3): after the compress
+// kernel on the same stream, copy the finished per-(frame, plane) SSE into
+// every peer's symmetric vector with P2P stores.  Folding this into the
+// issue-bound quant epilogue measured 19-22 % slower.
+__global__ void k_push_sse(const u64* __restrict__ sse, int64_t n, u64* const* __restrict__ peers,
+                           int n_peers, int64_t offset) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 v = sse[i];
+    for (int p = 0; p < n_peers; ++p) peers[p][offset + i] = v;
+  }
+  __threadfence_system();
+}
+
 // K3 for coarse tables whose quantiser still fits 16-bit lanes (every
 // Q' <= 8191, e.g. q = 10): the forward transform and the two-lane quantiser
 // run packed for two blocks (exact: |Z| <= 8192), dequantisation goes to
@@ -591,7 +598,6 @@ __device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
 
 constexpr size_t kHybridSmem = (size_t)64 * kThreads * sizeof(int) + (size_t)8 * kThreads * sizeof(uint4);
 
-template <bool XCHG>
 __global__ void __launch_bounds__(kThreads, 2)
     k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
   extern __shared__ uint4 s_dyn[];
@@ -668,8 +674,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       acc = sse4(wi.w, o.y, acc);
     }
   }
-  if (sse != nullptr)
-    warp_sse_add<kThreads, XCHG>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // K3 for coarse tables (wide == 1, e.g. q < 25): one block per thread.  The
@@ -726,8 +731,7 @@ __global__ void __launch_bounds__(kThreads)
       acc = sse4(w[i].y, hi, acc);
     }
   }
-  if (sse != nullptr)
-    warp_sse_add<kThreads>(acc, sse, L.frame * ps.n_planes + L.plane, ps.x, ps.p[L.plane].units);
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // ---------------------------------------------------------------------------

@@ -482,7 +482,7 @@ int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes, in
 
 // --- K3/K6 quant -------------------------------------------------------------
 static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
-                        uint64_t* sse, void* stream, const XchgDev* xchg);
+                        uint64_t* sse, void* stream, const void* unused);
 
 int adct_compress_quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames,
                                const adct_qtab_t* qtab, uint64_t* sse, void* stream) {
@@ -493,26 +493,23 @@ int adct_compress_quant_planes_exchange(const adct_plane_t* planes, int32_t n_pl
                                         const adct_qtab_t* qtab, uint64_t* sse, uint64_t* const* peer_sse,
                                         int32_t n_peers, int64_t peer_offset, uint32_t* arrivals,
                                         void* stream) {
+  (void)arrivals;  // not needed by the push form (kept for symmetry with the retain entry point)
   if (n_frames < 0 || n_peers < 1 || n_peers > 1024 || peer_offset < 0) return ADCT_ERR_INVALID_ARGUMENT;
   if (n_frames == 0) return quant_planes(planes, n_planes, 0, qtab, sse, stream, nullptr);
-  if (sse == nullptr || peer_sse == nullptr || arrivals == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
-  if (!aligned(sse, 8) || !aligned(peer_sse, 8) || !aligned(arrivals, 4)) return ADCT_ERR_MISALIGNED;
-  XchgDev x;
-  x.peers = reinterpret_cast<u64* const*>(peer_sse);
-  x.arrivals = arrivals;
-  x.offset = peer_offset;
-  x.n_peers = n_peers;
-  // packed arrival counting needs < 2^16 warps (256-unit tiles) per plane
-  x.packed = 1;
-  for (int k = 0; planes != nullptr && k < n_planes && k < 3; ++k) {
-    const int64_t units = (int64_t)planes[k].height / 8 * (planes[k].width / 8);  // upper bound (single-block units)
-    if ((units + 255) / 256 * 8 > 65535) x.packed = 0;
-  }
-  return quant_planes(planes, n_planes, n_frames, qtab, sse, stream, &x);
+  if (sse == nullptr || peer_sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  if (!aligned(sse, 8) || !aligned(peer_sse, 8)) return ADCT_ERR_MISALIGNED;
+  int rc = quant_planes(planes, n_planes, n_frames, qtab, sse, stream, nullptr);
+  if (rc != ADCT_OK) return rc;
+  const int64_t n = n_frames * n_planes;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  k_push_sse<<<blocks, 256, 0, as_stream(stream)>>>(reinterpret_cast<const u64*>(sse), n,
+                                                    reinterpret_cast<u64* const*>(peer_sse), n_peers, peer_offset);
+  ADCT_CUDA_TRY(cudaGetLastError());
+  return ADCT_OK;
 }
 
 static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
-                        uint64_t* sse, void* stream, const XchgDev* xchg) {
+                        uint64_t* sse, void* stream, const void* /*unused*/) {
   if (qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   for (int p = 0; p < 64; ++p)
     if (qtab->qprime[p] < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
@@ -521,7 +518,6 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
   PlaneSetHost ps;
   int rc = build_planes(planes, n_planes, n_frames, ps, wide);
   if (rc != ADCT_OK) return rc;
-  if (xchg != nullptr) ps.dev.x = *xchg;
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
@@ -532,12 +528,11 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
       PlaneSetHost ph;  // two blocks per thread where every plane pairs
       rc = build_planes(planes, n_planes, n_frames, ph, false);
       if (rc != ADCT_OK) return rc;
-      if (xchg != nullptr) ph.dev.x = *xchg;
       if (ph.pair) {
-        auto kh = xchg != nullptr ? k_quant_hybrid<true> : k_quant_hybrid<false>;
-        ADCT_CUDA_TRY(cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHybridSmem));
+        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kHybridSmem));
         return for_frame_chunks(ph, n_frames, [&](dim3 g) {
-          kh<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
+          k_quant_hybrid<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
         });
       }
     }
@@ -554,17 +549,11 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     if ((int64_t)grid > n_tiles) grid = (int)n_tiles;
     ps.dev.frame_base = 0;
     const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
-#define ADCT_QP(PA, FL)                                                                          \
-  do {                                                                                           \
-    if (xchg != nullptr) {                                                                       \
-      ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL, true>,                                \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      k_quant_p<PA, FL, true><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x); \
-    } else {                                                                                     \
-      ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL, false>,                               \
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      k_quant_p<PA, FL, false><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x); \
-    }                                                                                            \
+#define ADCT_QP(PA, FL)                                                                        \
+  do {                                                                                         \
+    ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL>,                                      \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_quant_p<PA, FL><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x);      \
   } while (0)
     if (ps.pair) {
       if (al) ADCT_QP(true, false); else ADCT_QP(true, true);
