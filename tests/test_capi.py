@@ -197,3 +197,38 @@ def test_error_mapping():
         _lib.check(3)
     with pytest.raises(RuntimeError):
         _lib.check(7)
+
+
+def test_qtab_random_tables_replay_exactly():
+    """Seeded random Q' tables over the supported range (1 .. 2^20, halves
+    included to exercise the rounding): the builder either reports the table
+    as packed-capable and the two-lane constants replay exactly, or marks it
+    wide; the scalar constants always replay exactly."""
+    rng = np.random.default_rng(7)
+    Z = np.arange(-8192, 8193, dtype=np.int64)
+    for _ in range(12):
+        scale = 10.0 ** rng.uniform(0, 6.3, size=(8, 8))
+        qpu = np.where(rng.random((8, 8)) < 0.2, np.floor(scale) + 0.5, scale)
+        qpu = np.minimum(qpu, 2.0**20)
+        t = quant.quant_table(qprime_unrounded=qpu)
+        Qp = quant.qtab_qprime(t).reshape(64)
+        assert (Qp == np.maximum(1, np.floor(qpu.reshape(64) + 0.5))).all()
+        want = np.sign(Z)[None, :] * ((2 * np.abs(Z)[None, :] + Qp[:, None]) // (2 * Qp[:, None]))
+        mag_w = np.frombuffer(bytes(t.magic_w), dtype=np.uint32).astype(np.uint64)
+        cadd = np.frombuffer(bytes(t.cadd_w), dtype=np.int32).astype(np.int64)
+        kw = np.frombuffer(bytes(t.kw), dtype=np.int32).astype(np.int64)
+        U = (2 * Z - (Z < 0))[None, :] + cadd[:, None]
+        got = ((U.astype(np.uint64) * mag_w[:, None]) >> np.uint64(32)).astype(np.int64) - kw[:, None]
+        assert np.array_equal(got, want)
+        mult = np.frombuffer(bytes(t.mult), dtype=np.int32).astype(np.int64)
+        packed = mult != 0
+        if packed.any():
+            mag = np.frombuffer(bytes(t.magic), dtype=np.uint32).astype(np.uint64)[packed]
+            bias = np.frombuffer(bytes(t.bias), dtype=np.int32).astype(np.int64)[packed]
+            kq = np.frombuffer(bytes(t.kq), dtype=np.int32).astype(np.int64)[packed]
+            Up = (Z[None, :] + bias[:, None]) * mult[packed][:, None] + (Z >= 0)[None, :]
+            assert Up.min() >= 0 and Up.max() <= 0xFFFF
+            gotp = ((Up.astype(np.uint64) * mag[:, None]) >> np.uint64(32)).astype(np.int64) - kq[:, None]
+            assert np.array_equal(gotp, want[packed])
+        if not packed.all():
+            assert t.wide == 1

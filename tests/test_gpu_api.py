@@ -159,6 +159,27 @@ def test_host_pipeline_planes(cuda, chunk):
             assert np.array_equal(sse_only[:, k], ws)
 
 
+def test_host_pipeline_empty_and_degenerate(cuda):
+    """Zero images / frames and zero-size planes are no-ops with well-formed results."""
+    from paper_1702_00817_b200 import errors
+
+    with HostPipeline(0) as p:
+        e = np.empty((0, 64, 64), np.uint8)
+        _, sse = p.compress_retain(e, 10, np.empty_like(e))
+        assert sse.shape == (0,)
+        _, sseq = p.compress_quant(e, quant.quant_table(50))
+        assert sseq.shape == (0,)
+        outs, ssep = p.compress_quant_planes([e, np.empty((0, 32, 32), np.uint8)], quant.quant_table(50))
+        assert ssep.shape == (0, 2)
+        z = np.empty((3, 0, 8), np.uint8)  # zero-height images: exact zero SSE, nothing transferred
+        _, sz = p.compress_retain(z, 10)
+        assert np.array_equal(sz, np.zeros(3, np.int64))
+        with pytest.raises(errors.BadDimensions):
+            p.compress_retain(np.zeros((1, 12, 16), np.uint8), 10)
+        with pytest.raises(errors.InvalidRetention):
+            p.compress_retain(np.zeros((1, 8, 16), np.uint8), 65)
+
+
 def test_pinned_empty_buffers_through_pipeline(cuda):
     import gc
 
