@@ -459,86 +459,66 @@ def gpu_arm(args) -> None:
     peak, peak_src = measured_hbm_peak()
 
     # ---- end to end: host buffers through the C-ABI pipeline (every rank) -------
+    def timed_e2e(call, outs):
+        """Mean wall time of 3 host-pipeline calls after one warm call; max over ranks."""
+        call(outs)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            call(outs)
+        dt = (time.perf_counter() - t0) / 3
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        return dt
+
     e2e = None
-    if not args.no_e2e and cfg["kind"] == "planes":
-        # frames of host planes through adct_pipeline_compress_quant_planes
-        m = min(per, max(1, args.e2e_images // 4))
-        host_in = [pinned_empty((m,) + tuple(p.shape[1:])) for p in planes]
-        host_out = [pinned_empty(a.shape) for a in host_in]
-        for a, p in zip(host_in, planes):
-            a[...] = p[:m].cpu().numpy()
-        qt4 = quant.quant_table(cfg["q"])
+    if not args.no_e2e and cfg["kind"] in ("retain", "quant", "planes"):
+        # page-locked host buffers from adct_host_alloc (cudaHostAlloc), filled
+        # from the device copies before the timed region
+        if cfg["kind"] == "planes":  # frames of Y/Cb/Cr host planes
+            m = min(per, max(1, args.e2e_images // 4))
+            host_in = [pinned_empty((m,) + tuple(p.shape[1:])) for p in planes]
+            for a, p in zip(host_in, planes):
+                a[...] = p[:m].cpu().numpy()
+            host_out = [pinned_empty(a.shape) for a in host_in]
+            n_sse = 3 * m
+            qt4 = quant.quant_table(cfg["q"])
+            chunk = max(args.e2e_chunk_mb << 20, 2 * sum(a[0].nbytes for a in host_in))
+            api = "adct_pipeline_compress_quant_planes (C ABI) via paper_1702_00817_b200.pipeline"
+            units = {"frames_per_step": world * m}
+        else:
+            m = min(per, args.e2e_images)
+            host_in = [pinned_empty(tuple(imgs[:m].shape))]
+            host_in[0][...] = imgs[:m].cpu().numpy()
+            host_out = [pinned_empty(host_in[0].shape)]
+            n_sse = m
+            qt0 = quant.quant_table(cfg["q"][0]) if cfg["kind"] == "quant" else None
+            chunk = args.e2e_chunk_mb << 20
+            api = "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline"
+            units = {"images_per_step": world * m}
         try:
-            with HostPipeline(local, chunk_bytes=max(args.e2e_chunk_mb << 20, 2 * sum(a[0].nbytes for a in host_in))) as pipe:
-                def timed_planes(outs):
-                    pipe.compress_quant_planes(host_in, qt4, outs, register=False)
-                    if world > 1:
-                        dist.barrier()
-                    t0 = time.perf_counter()
-                    for _ in range(3):
-                        pipe.compress_quant_planes(host_in, qt4, outs, register=False)
-                    dt = (time.perf_counter() - t0) / 3
-                    if world > 1:
-                        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                        dt = t.item()
-                    return dt
-                dt = timed_planes(host_out)
-                dt_metric = timed_planes(None)
+            with HostPipeline(local, chunk_bytes=chunk) as pipe:
+                if cfg["kind"] == "planes":
+                    call = lambda outs: pipe.compress_quant_planes(host_in, qt4, outs, register=False)
+                elif cfg["kind"] == "retain":
+                    call = lambda outs: pipe.compress_retain(host_in[0], cfg["r"], outs and outs[0], register=False)
+                else:
+                    call = lambda outs: pipe.compress_quant(host_in[0], qt0, outs and outs[0], register=False)
+                dt = timed_e2e(call, host_out)  # reconstructions come back to the host every step
+                dt_metric = timed_e2e(call, None)  # inputs in, per-image SSE (-> PSNR) back
             px = world * sum(a.size for a in host_in)
             nbytes = sum(a.nbytes for a in host_in)
             e2e = {"value": px / dt / 1e9, "unit": UNIT,
                    "h2d_bytes_per_step": int(world * nbytes),
-                   "d2h_bytes_per_step": int(world * (nbytes + 8 * 3 * m)),
-                   "frames_per_step": world * m,
-                   "api": "adct_pipeline_compress_quant_planes (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks",
+                   "d2h_bytes_per_step": int(world * (nbytes + 8 * n_sse)),
+                   **units,
+                   "api": api + ", every rank, max time over ranks",
                    "metric_only": {"value": px / dt_metric / 1e9, "unit": UNIT,
                                    "h2d_bytes_per_step": int(world * nbytes),
-                                   "d2h_bytes_per_step": int(world * 8 * 3 * m),
-                                   "note": "reconstructions kept on the device; only the per-frame, per-plane SSE is read back"}}
-        finally:
-            del host_in, host_out
-    if not args.no_e2e and cfg["kind"] in ("retain", "quant"):
-        m = min(per, args.e2e_images)
-        # page-locked host buffers from adct_host_alloc (cudaHostAlloc); the
-        # input batch is filled from the device copy before the timed region
-        host_in = pinned_empty(tuple(imgs[:m].shape))
-        host_out = pinned_empty(host_in.shape)
-        host_in[...] = imgs[:m].cpu().numpy()
-        try:
-            with HostPipeline(local, chunk_bytes=args.e2e_chunk_mb << 20) as pipe:
-                if cfg["kind"] == "retain":
-                    call = lambda rec: pipe.compress_retain(host_in, cfg["r"], rec, register=False)
-                else:
-                    qt0 = quant.quant_table(cfg["q"][0])
-                    call = lambda rec: pipe.compress_quant(host_in, qt0, rec, register=False)
-
-                def timed(rec):
-                    call(rec)
-                    reps = 3
-                    if world > 1:
-                        dist.barrier()
-                    t0 = time.perf_counter()
-                    for _ in range(reps):
-                        call(rec)
-                    dt = (time.perf_counter() - t0) / reps
-                    if world > 1:
-                        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                        dt = t.item()
-                    return dt
-
-                dt = timed(host_out)  # reconstructions come back to the host every step
-                dt_metric = timed(None)  # inputs in, per-image SSE (-> PSNR) back
-            px = world * m * cfg["h"] * cfg["w"]
-            e2e = {"value": px / dt / 1e9, "unit": UNIT,
-                   "h2d_bytes_per_step": int(world * host_in.nbytes),
-                   "d2h_bytes_per_step": int(world * (host_out.nbytes + 8 * m)),
-                   "images_per_step": world * m,
-                   "api": "adct_pipeline_compress_* (C ABI) via paper_1702_00817_b200.pipeline, every rank, max time over ranks",
-                   "metric_only": {"value": px / dt_metric / 1e9, "unit": UNIT,
-                                   "h2d_bytes_per_step": int(world * host_in.nbytes),
-                                   "d2h_bytes_per_step": int(world * 8 * m),
+                                   "d2h_bytes_per_step": int(world * 8 * n_sse),
                                    "note": "reconstructions kept on the device; only the SSE/PSNR vector is read back"}}
         finally:
             del host_in, host_out
