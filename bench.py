@@ -405,10 +405,10 @@ def gpu_arm(args) -> None:
         step()
     torch.cuda.synchronize()
     graphed = False
-    if cfg["kind"] in ("sweep", "forward") and not args.no_graph:
-        # launch-bound configs (one small launch per step): replay the step's
-        # C-ABI launch from a CUDA graph so host-side call overhead does not
-        # leave the GPU idle between steps
+    if cfg["kind"] in ("sweep", "forward", "quant") and not args.no_graph:
+        # short launches (configs 0/1: one small launch; config 2: three
+        # ~0.16 ms launches per step): replay the step's C-ABI launches from a
+        # CUDA graph so host-side call overhead does not leave the GPU idle
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step_kernel()
@@ -581,7 +581,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-graph", action="store_true", help="configs 0/1: launch through the C ABI every step")
+    ap.add_argument("--no-graph", action="store_true", help="configs 0/1/2: launch through the C ABI every step")
     ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "fused"],
                     help="configs 3 and 4: SSE exchange by NCCL all-reduce (default) or fused into the kernel "
                          "epilogue through torch symmetric memory")
