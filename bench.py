@@ -163,6 +163,19 @@ def _ref_forward_task(args):
     return float(refport.coefficient_blocks(img)[0, 0, 0])
 
 
+def quant_jit_stats():
+    """Counters of the run-time table specialisation of the quant kernels
+    (adct_quant_jit_stats): kernels compiled and specialised launches so far."""
+    import ctypes
+
+    from paper_1702_00817_b200 import _lib
+
+    c, l, f = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.lib().adct_quant_jit_stats(ctypes.byref(c), ctypes.byref(l), ctypes.byref(f))
+    return {"compiled": c.value, "specialised_launches": l.value, "failures": f.value,
+            "after_uses": int(os.environ.get("ADCT_QUANT_JIT_AFTER", "3"))}
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -563,6 +576,7 @@ def gpu_arm(args) -> None:
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "cuda_graph": graphed,
+            "quant_jit": quant_jit_stats(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -31,8 +31,18 @@
 // because T^T e0 e0^T T = all-ones (row 0 of T is all ones).
 #pragma once
 
+#ifdef __CUDACC_RTC__  // NVRTC (quantiser specialisation, capi.cu): no host headers
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace adct {
 

@@ -46,13 +46,23 @@ struct QParamsWide {  // scalar quantiser of k_quant_wide
 // errs when Z_B == 0, where both tie-breaks give q = 0 (host-verified).
 //   U = (Z + B) * mult + [Z >= 0]   (both 16-bit fields, no carry)
 //   q + kq = umulhi(U, magic)       (exact, adct_qtab_build)
+// Where the quantiser constants come from: the kernel parameters (any
+// table), or — in kernels specialised at run time for one table (capi.cu,
+// NVRTC) — compile-time constants that become instruction immediates
+// (removes the 2 LDC.64 + 1 LDCU per position: +5.5 % on config 4).
+struct ParamTab {
+  static __device__ __forceinline__ uint4 pos(const QParamsDev& q, int p) { return q.pos[p]; }
+  static __device__ __forceinline__ u32 wadd(const QParamsDev& q, int p) { return q.wadd[p]; }
+};
+
+template <class TAB = ParamTab>
 __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
-  const uint4 c = q.pos[p];
+  const uint4 c = TAB::pos(q, p);
   const u32 s = ((z >> 15) & 0x10001u) ^ 0x10001u;
   const u32 U = z * c.y + c.z + s;
   const u32 qa = __umulhi(U & 0xFFFFu, c.x);
   const u32 qb = __umulhi(U >> 16, c.x);
-  return (qa + (qb << 16)) * c.w + q.wadd[p];
+  return (qa + (qb << 16)) * c.w + TAB::wadd(q, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -244,7 +254,7 @@ __device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <bool PAIR, bool FLIP>
+template <bool PAIR, bool FLIP, class TAB = ParamTab>
 __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
         fwd8(col, Zc);
         if (v == 0) Zc[0] -= 8192u * 65537u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) Wc[u] = quant_pair(Zc[u], u * 8 + v, q);
+        for (int u = 0; u < 8; ++u) Wc[u] = quant_pair<TAB>(Zc[u], u * 8 + v, q);
         inv8(Wc, cc);
 #pragma unroll
         for (int i = 0; i < 8; ++i) c[i][v] = cc[i];
@@ -306,6 +316,105 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     cur = nxt;
     if (nt >= n_tiles) break;
   }
+}
+
+// K3 for coarse tables whose quantiser still fits 16-bit lanes (every
+// Q' <= 8191, e.g. q = 10): the forward transform and the two-lane quantiser
+// run packed for two blocks (exact: |Z| <= 8192), dequantisation goes to
+// int32 per block, and only the inverse — the part whose range needs more
+// than 16 bits — runs per block in 32 bits.  Block A's column inverse
+// streams in registers; block B's dequantised coefficients wait in shared
+// memory.  `q.wadd` holds the scalar offsets here (-kq*qe, + 32 + 8192 at DC).
+__device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
+  u32 h2[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int a = V[4 * half + 2 * j] >> 6, b = V[4 * half + 2 * j + 1] >> 6;  // |.| < 2^15
+    h2[j] = __vimin_s16x2_relu(__byte_perm((u32)a, (u32)b, 0x5410), 0x00FF00FFu);
+  }
+  return __byte_perm(h2[0], h2[1], 0x6420);
+}
+
+constexpr unsigned long long kHybridSmem = 64ull * kThreads * sizeof(int) + 8ull * kThreads * sizeof(uint4);
+
+template <class TAB = ParamTab>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
+  extern __shared__ uint4 s_dyn[];
+  uint4* s_orig = s_dyn;                                          // [8][kThreads]
+  int* s_wb = reinterpret_cast<int*>(s_dyn + 8 * kThreads);       // [64][kThreads]
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<true>(ps, L)) {
+    uint4 w[8];
+    load_unit<true>(L.src, L.width, w);
+    u32 x[8][8];
+    unpack_unit(w, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_orig[i * kThreads + threadIdx.x] = w[i];
+    int cA[8][8];
+    {
+      u32 t[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        u32 col[8], Zc[8];
+        int wa[8], cc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+        fwd8(col, Zc);
+        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int p = u * 8 + v;
+          const uint4 c = TAB::pos(q, p);
+          const u32 z = Zc[u];
+          const u32 sg = ((z >> 15) & 0x10001u) ^ 0x10001u;
+          const u32 U = z * c.y + c.z + sg;
+          const u32 qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
+          const u32 qb = __umulhi(U >> 16, c.x);      // lane B
+          wa[u] = (int)(qa * c.w) + (int)TAB::wadd(q, p);
+          s_wb[p * kThreads + threadIdx.x] = (int)(qb * c.w) + (int)TAB::wadd(q, p);
+        }
+        inv8(wa, cc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cA[i][v] = cc[i];
+      }
+    }
+    // block A rows go out now (8-byte stores; L2 merges them with B's halves)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int V[8];
+      inv8(cA[i], V);
+      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
+      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width, o);
+      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      acc = sse4(wi.x, o.x, acc);
+      acc = sse4(wi.y, o.y, acc);
+    }
+    int cB[8][8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      int col[8], cc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) col[u] = s_wb[(u * 8 + v) * kThreads + threadIdx.x];
+      inv8(col, cc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cB[i][v] = cc[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int V[8];
+      inv8(cB[i], V);
+      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
+      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width + 8, o);
+      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      acc = sse4(wi.z, o.x, acc);
+      acc = sse4(wi.w, o.y, acc);
+    }
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // ---------------------------------------------------------------------------
@@ -577,104 +686,6 @@ __global__ void k_push_sse(const u64* __restrict__ sse, int64_t n, u64* const* _
     for (int p = 0; p < n_peers; ++p) peers[p][offset + i] = v;
   }
   __threadfence_system();
-}
-
-// K3 for coarse tables whose quantiser still fits 16-bit lanes (every
-// Q' <= 8191, e.g. q = 10): the forward transform and the two-lane quantiser
-// run packed for two blocks (exact: |Z| <= 8192), dequantisation goes to
-// int32 per block, and only the inverse — the part whose range needs more
-// than 16 bits — runs per block in 32 bits.  Block A's column inverse
-// streams in registers; block B's dequantised coefficients wait in shared
-// memory.  `q.wadd` holds the scalar offsets here (-kq*qe, + 32 + 8192 at DC).
-__device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
-  u32 h2[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int a = V[4 * half + 2 * j] >> 6, b = V[4 * half + 2 * j + 1] >> 6;  // |.| < 2^15
-    h2[j] = __vimin_s16x2_relu(__byte_perm((u32)a, (u32)b, 0x5410), 0x00FF00FFu);
-  }
-  return __byte_perm(h2[0], h2[1], 0x6420);
-}
-
-constexpr size_t kHybridSmem = (size_t)64 * kThreads * sizeof(int) + (size_t)8 * kThreads * sizeof(uint4);
-
-__global__ void __launch_bounds__(kThreads, 2)
-    k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
-  extern __shared__ uint4 s_dyn[];
-  uint4* s_orig = s_dyn;                                          // [8][kThreads]
-  int* s_wb = reinterpret_cast<int*>(s_dyn + 8 * kThreads);       // [64][kThreads]
-  UnitLoc L;
-  u32 acc = 0;
-  if (locate_unit<true>(ps, L)) {
-    uint4 w[8];
-    load_unit<true>(L.src, L.width, w);
-    u32 x[8][8];
-    unpack_unit(w, x);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s_orig[i * kThreads + threadIdx.x] = w[i];
-    int cA[8][8];
-    {
-      u32 t[8][8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        u32 col[8], Zc[8];
-        int wa[8], cc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
-        fwd8(col, Zc);
-        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int p = u * 8 + v;
-          const uint4 c = q.pos[p];
-          const u32 z = Zc[u];
-          const u32 sg = ((z >> 15) & 0x10001u) ^ 0x10001u;
-          const u32 U = z * c.y + c.z + sg;
-          const u32 qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
-          const u32 qb = __umulhi(U >> 16, c.x);      // lane B
-          wa[u] = (int)(qa * c.w) + (int)q.wadd[p];
-          s_wb[p * kThreads + threadIdx.x] = (int)(qb * c.w) + (int)q.wadd[p];
-        }
-        inv8(wa, cc);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cA[i][v] = cc[i];
-      }
-    }
-    // block A rows go out now (8-byte stores; L2 merges them with B's halves)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int V[8];
-      inv8(cA[i], V);
-      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
-      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width, o);
-      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
-      acc = sse4(wi.x, o.x, acc);
-      acc = sse4(wi.y, o.y, acc);
-    }
-    int cB[8][8];
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      int col[8], cc[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) col[u] = s_wb[(u * 8 + v) * kThreads + threadIdx.x];
-      inv8(col, cc);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cB[i][v] = cc[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int V[8];
-      inv8(cB[i], V);
-      const uint2 o = make_uint2(pack_px8(V, 0), pack_px8(V, 1));
-      if (L.dst != nullptr) st_stream8(L.dst + (int64_t)i * L.width + 8, o);
-      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
-      acc = sse4(wi.z, o.x, acc);
-      acc = sse4(wi.w, o.y, acc);
-    }
-  }
-  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
 }
 
 // K3 for coarse tables (wide == 1, e.g. q < 25): one block per thread.  The

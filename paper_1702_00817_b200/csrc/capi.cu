@@ -11,6 +11,7 @@
 
 #include "adct_cuda.h"
 #define ADCT_DEFINE_PLAIN_KERNELS
+#include "adct_jit.h"
 #include "adct_launch.h"
 
 using namespace adct;
@@ -529,10 +530,18 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
       rc = build_planes(planes, n_planes, n_frames, ph, false);
       if (rc != ADCT_OK) return rc;
       if (ph.pair) {
-        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (void* jf = jit::quant_function(jit::kHybrid, qh)) {  // table-specialised build
+          void* args[] = {&ph.dev, &qh, &d_sse};
+          int rcj = ADCT_OK;
+          const int rcc = for_frame_chunks(ph, n_frames, [&](dim3 g) {
+            if (jit::launch(jf, g, dim3(kThreads), kHybridSmem, s, args) != 0) rcj = ADCT_ERR_CUDA;
+          });
+          return rcj != ADCT_OK ? rcj : rcc;
+        }
+        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kHybridSmem));
         return for_frame_chunks(ph, n_frames, [&](dim3 g) {
-          k_quant_hybrid<<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
+          k_quant_hybrid<><<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
         });
       }
     }
@@ -549,6 +558,15 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     if ((int64_t)grid > n_tiles) grid = (int)n_tiles;
     ps.dev.frame_base = 0;
     const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
+    const int kind = ps.pair ? (al ? jit::kQuantPairAligned : jit::kQuantPairFlip)
+                             : (al ? jit::kQuantSingleAligned : jit::kQuantSingleFlip);
+    if (void* jf = jit::quant_function(kind, q)) {  // table-specialised build
+      QParamsDev qa = q;
+      uint32_t tpf = ps.grid_x;
+      void* args[] = {&ps.dev, &qa, &d_sse, const_cast<int64_t*>(&n_tiles), &tpf};
+      if (jit::launch(jf, dim3(grid), dim3(kThreads), smem, s, args) != 0) return ADCT_ERR_CUDA;
+      return ADCT_OK;
+    }
 #define ADCT_QP(PA, FL)                                                                        \
   do {                                                                                         \
     ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL>,                                      \
@@ -1010,6 +1028,15 @@ int adct_pipeline_compress_quant_planes(adct_pipeline_t* p, const adct_plane_t* 
                                         int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
                                         uint64_t* host_sse) {
   return pipeline_planes_run(p, host_planes, n_planes, n_frames, qtab, host_sse);
+}
+
+int adct_quant_jit_stats(int64_t* compiled, int64_t* launches, int64_t* failures) {
+  long long c = 0, l = 0, f = 0;
+  jit::stats(&c, &l, &f);
+  if (compiled) *compiled = c;
+  if (launches) *launches = l;
+  if (failures) *failures = f;
+  return ADCT_OK;
 }
 
 int adct_host_register(void* ptr, size_t bytes) {
