@@ -51,6 +51,7 @@ struct QParamsWide {  // scalar quantiser of k_quant_wide
 // NVRTC) — compile-time constants that become instruction immediates
 // (removes the 2 LDC.64 + 1 LDCU per position: +5.5 % on config 4).
 struct ParamTab {
+  static constexpr bool kBaked = false;  // constants unknown at compile time
   static __device__ __forceinline__ uint4 pos(const QParamsDev& q, int p) { return q.pos[p]; }
   static __device__ __forceinline__ u32 wadd(const QParamsDev& q, int p) { return q.wadd[p]; }
 };
@@ -58,7 +59,9 @@ struct ParamTab {
 template <class TAB = ParamTab>
 __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
   const uint4 c = TAB::pos(q, p);
-  const u32 s = ((z >> 15) & 0x10001u) ^ 0x10001u;
+  // mult == 2 <=> odd Q': no ties, so the sign term never matters (the host
+  // check verifies both values); a specialised kernel drops it there
+  const u32 s = (TAB::kBaked && c.y == 2u) ? 0u : ((z >> 15) & 0x10001u) ^ 0x10001u;
   const u32 U = z * c.y + c.z + s;
   const u32 qa = __umulhi(U & 0xFFFFu, c.x);
   const u32 qb = __umulhi(U >> 16, c.x);
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int p = u * 8 + v;
           const uint4 c = TAB::pos(q, p);
           const u32 z = Zc[u];
-          const u32 sg = ((z >> 15) & 0x10001u) ^ 0x10001u;
+          const u32 sg = (TAB::kBaked && c.y == 2u) ? 0u : ((z >> 15) & 0x10001u) ^ 0x10001u;
           const u32 U = z * c.y + c.z + sg;
           const u32 qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
           const u32 qb = __umulhi(U >> 16, c.x);      // lane B

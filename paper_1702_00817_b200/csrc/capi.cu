@@ -257,7 +257,11 @@ int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out
       for (int64_t Z = -kZmax; ok && Z <= kZmax; ++Z) {
         // s = [Z >= 0]; at Z == 0 the kernel's lane-B sign bit may read 1
         // (borrow from a negative lane A), so both values must agree there.
-        for (int s = (Z == 0 ? 0 : (Z > 0 ? 1 : 0)); s <= (Z >= 0 ? 1 : 0); ++s) {
+        // odd Q': both s values for every Z (2Z + Q' is odd, so no tie exists
+        // and s never matters) — specialised kernels drop s there
+        const int s_lo = odd ? 0 : (Z == 0 ? 0 : (Z > 0 ? 1 : 0));
+        const int s_hi = odd ? 1 : (Z >= 0 ? 1 : 0);
+        for (int s = s_lo; s <= s_hi; ++s) {
           const int64_t U = (Z + B) * mult + s;
           if (U < 0 || U > 0xFFFF) { ok = false; break; }
           const int64_t got = (int64_t)(((uint64_t)U * m) >> 32) - K1;

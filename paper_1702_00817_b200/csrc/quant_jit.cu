@@ -137,7 +137,7 @@ const char* kernel_expression(int kind) {
 }
 
 std::string baked_source(const QParamsDev& q) {
-  std::string s = "#include \"adct_kernels.cuh\"\nstruct BakedTab {\n";
+  std::string s = "#include \"adct_kernels.cuh\"\nstruct BakedTab {\n  static constexpr bool kBaked = true;\n";
   s += "  static __device__ __forceinline__ uint4 pos(const adct::QParamsDev&, int p) {\n";
   s += "    constexpr unsigned t[64][4] = {";
   char buf[96];
