@@ -200,8 +200,11 @@ CUfunction build(int kind, const QParamsDev& q) {
 void* quant_function(int kind, const QParamsDev& q) {
   const int after = threshold();
   if (after <= 0) return nullptr;
+  int dev = 0;  // a loaded module belongs to one device's context: key by device too
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::string key(reinterpret_cast<const char*>(&q), sizeof(QParamsDev));
   key.push_back((char)kind);
+  key.append(reinterpret_cast<const char*>(&dev), sizeof dev);
   std::lock_guard<std::mutex> lock(g_mu);
   Entry& e = g_cache[key];
   if (e.state == 1) return e.fn;
