@@ -534,7 +534,7 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
       rc = build_planes(planes, n_planes, n_frames, ph, false);
       if (rc != ADCT_OK) return rc;
       if (ph.pair) {
-        if (void* jf = jit::quant_function(jit::kHybrid, qh)) {  // table-specialised build
+        if (void* jf = jit::quant_function(jit::kHybrid, qh, s)) {  // table-specialised build
           void* args[] = {&ph.dev, &qh, &d_sse};
           int rcj = ADCT_OK;
           const int rcc = for_frame_chunks(ph, n_frames, [&](dim3 g) {
@@ -564,7 +564,7 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
     const int kind = ps.pair ? (al ? jit::kQuantPairAligned : jit::kQuantPairFlip)
                              : (al ? jit::kQuantSingleAligned : jit::kQuantSingleFlip);
-    if (void* jf = jit::quant_function(kind, q)) {  // table-specialised build
+    if (void* jf = jit::quant_function(kind, q, s)) {  // table-specialised build
       QParamsDev qa = q;
       uint32_t tpf = ps.grid_x;
       void* args[] = {&ps.dev, &qa, &d_sse, const_cast<int64_t*>(&n_tiles), &tpf};

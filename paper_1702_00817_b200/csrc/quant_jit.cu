@@ -197,9 +197,13 @@ CUfunction build(int kind, const QParamsDev& q) {
 
 }  // namespace
 
-void* quant_function(int kind, const QParamsDev& q) {
+void* quant_function(int kind, const QParamsDev& q, cudaStream_t stream) {
   const int after = threshold();
   if (after <= 0) return nullptr;
+  // never build while `stream` is being captured into a CUDA graph (module
+  // loading is not a capturable operation); a kernel built earlier is fine
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
   int dev = 0;  // a loaded module belongs to one device's context: key by device too
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::string key(reinterpret_cast<const char*>(&q), sizeof(QParamsDev));
@@ -208,7 +212,7 @@ void* quant_function(int kind, const QParamsDev& q) {
   std::lock_guard<std::mutex> lock(g_mu);
   Entry& e = g_cache[key];
   if (e.state == 1) return e.fn;
-  if (e.state < 0) return nullptr;
+  if (e.state < 0 || capturing) return nullptr;
   if (++e.uses < after) return nullptr;
   e.fn = build(kind, q);
   e.state = e.fn ? 1 : -1;

@@ -62,3 +62,36 @@ def test_specialised_kernels_are_exact():
 
 def test_specialisation_off():
     assert _run(0) == (0, 0, 0)
+
+
+def test_first_use_inside_graph_capture():
+    """A table first seen while the stream is being captured keeps the generic
+    kernel in the graph (no module load during capture); the replay is exact
+    and the next uncaptured call specialises."""
+    code = r'''
+import ctypes, numpy as np, torch
+from oracle import exact
+from paper_1702_00817_b200 import batch, quant, synth, _lib
+dev = torch.device("cuda", 0)
+x = synth.config_images_device(2, [5], device=dev)[:, :128, :256].contiguous()
+qt = quant.quant_table(75)
+rec = torch.empty_like(x); sse = torch.empty(1, dtype=torch.int64, device=dev)
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    with torch.cuda.graph(g):
+        batch.compress_quant(x, qt, out=rec, sse_out=sse)
+g.replay(); torch.cuda.synchronize()
+wr, ws = exact.compress_quant(x.cpu().numpy(), quant.qtab_qprime(qt))
+assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws)
+batch.compress_quant(x, qt, out=rec, sse_out=sse); torch.cuda.synchronize()
+assert np.array_equal(rec.cpu().numpy(), wr)
+c, l, f = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+_lib.lib().adct_quant_jit_stats(ctypes.byref(c), ctypes.byref(l), ctypes.byref(f))
+print("STATS", c.value, l.value, f.value)
+'''
+    env = dict(os.environ, PYTHONPATH=ROOT, ADCT_QUANT_JIT_AFTER="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    compiled, launches, failures = (int(v) for v in r.stdout.split("STATS")[1].split())
+    assert failures == 0 and compiled == 1 and launches == 1
