@@ -561,8 +561,8 @@ __global__ void __launch_bounds__(kSweepThreads)
 #pragma unroll 1
   for (int r = 1; r <= r_max; ++r) {
     const int p = c_sweep.zz[r - 1];
-    const int u = p >> 3, v = p & 7;
     const u32 z = zs[p][threadIdx.x];
+    const int u = p >> 3, v = p & 7;
     const int4 a0 = c_sweep.t[u][0], a1 = c_sweep.t[u][1];
     const int4 b0 = c_sweep.t[v][0], b1 = c_sweep.t[v][1];
     const int a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
