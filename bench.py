@@ -499,7 +499,7 @@ def gpu_arm(args) -> None:
             host_out = [pinned_empty(a.shape) for a in host_in]
             n_sse = 3 * m
             qt4 = quant.quant_table(cfg["q"])
-            chunk = max(args.e2e_chunk_mb << 20, 2 * sum(a[0].nbytes for a in host_in))
+            chunk = max(args.e2e_chunk_mb << 20, 5 * sum(a[0].nbytes for a in host_in))  # ~5 frames: measured best
             api = "adct_pipeline_compress_quant_planes (C ABI) via paper_1702_00817_b200.pipeline"
             units = {"frames_per_step": world * m}
         else:
