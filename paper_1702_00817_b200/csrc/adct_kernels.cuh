@@ -529,9 +529,9 @@ __host__ __device__ constexpr SweepTables make_sweep_tables() {
 }
 __constant__ SweepTables c_sweep = make_sweep_tables();
 
-template <bool PAIR>
+template <bool PAIR, bool FSSE = false>
 __global__ void __launch_bounds__(kSweepThreads)
-    k_sweep_inc(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse) {
+    k_sweep_inc(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse, u64* __restrict__ ssef = nullptr) {
   __shared__ u32 zs[64][kSweepThreads];
   UnitLoc L;
   const bool active = locate_unit<PAIR, kSweepThreads>(ps, L);
@@ -576,6 +576,7 @@ __global__ void __launch_bounds__(kSweepThreads)
       for (int j = 0; j < 8; ++j) U[i][j] += (u32)a[i] * bz[j];
     if (r >= r_min) {
       u32 acc = 0;
+      u64 accf = 0;
       if (active) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -587,9 +588,32 @@ __global__ void __launch_bounds__(kSweepThreads)
             acc = sse4(w[i].z, o.z, acc);
             acc = sse4(w[i].w, o.w, acc);
           }
+          if (FSSE) {
+            // the reference's unrounded convention, row by row from the input
+            // words: sum (64 x - clamp(64 x_hat, 0, 16320))^2, 64 x_hat = U - 24608
+            const u32 p01 = __byte_perm(w[i].x, w[i].z, 0x5410), p23 = __byte_perm(w[i].x, w[i].z, 0x7632);
+            const u32 p45 = __byte_perm(w[i].y, w[i].w, 0x5410), p67 = __byte_perm(w[i].y, w[i].w, 0x7632);
+            const u32 xr[8] = {__byte_perm(p01, 0u, 0x4240), __byte_perm(p01, 0u, 0x4341),
+                               __byte_perm(p23, 0u, 0x4240), __byte_perm(p23, 0u, 0x4341),
+                               __byte_perm(p45, 0u, 0x4240), __byte_perm(p45, 0u, 0x4341),
+                               __byte_perm(p67, 0u, 0x4240), __byte_perm(p67, 0u, 0x4341)};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const u32 c = __vmaxu2(__vminu2(U[i][j], 0x9FE09FE0u), 0x60206020u);
+              const u32 d = (xr[j] << 6) + 0x60206020u - c;
+              const int da = (int)(d << 16) >> 16;
+              const int db = (int)(d - (u32)da) >> 16;
+              accf += (u64)(da * da) + (PAIR ? (u64)(db * db) : 0ull);
+            }
+          }
         }
       }
       block_add_u32(acc, out + (r - r_min));
+      if (FSSE) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) accf += __shfl_xor_sync(0xffffffffu, accf, o);
+        if ((threadIdx.x & 31) == 0 && accf != 0) atomicAdd(ssef + L.frame * nr + (r - r_min), accf);
+      }
     }
   }
 }

@@ -622,13 +622,18 @@ int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, i
   if (nsse && sse_unrounded) ADCT_CUDA_TRY(cudaMemsetAsync(sse_unrounded, 0, nsse * sizeof(uint64_t), s));
   u64* d_sse = reinterpret_cast<u64*>(sse);
   u64* d_ssef = reinterpret_cast<u64*>(sse_unrounded);
-  if (d_ssef == nullptr && sweep_kernel_choice() == 1) {  // rounded SSE only: incremental form
+  if (sweep_kernel_choice() == 1) {  // incremental form
     PlaneSetHost ps2;
     rc = build_planes(&pl, 1, n, ps2, false, kSweepThreads);
     if (rc != ADCT_OK) return rc;
     return for_frame_chunks(ps2, n, [&](dim3 g) {
-      if (ps2.pair) k_sweep_inc<true><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse);
-      else k_sweep_inc<false><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse);
+      if (d_ssef != nullptr) {
+        if (ps2.pair) k_sweep_inc<true, true><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse, d_ssef);
+        else k_sweep_inc<false, true><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse, d_ssef);
+      } else {
+        if (ps2.pair) k_sweep_inc<true><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse);
+        else k_sweep_inc<false><<<g, kSweepThreads, 0, s>>>(ps2.dev, r_min, r_max, d_sse);
+      }
     });
   }
   return for_frame_chunks(ps, n, [&](dim3 g) {

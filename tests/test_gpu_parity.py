@@ -190,7 +190,9 @@ def test_sweep_shapes_and_ranges(cuda, shape, r_min, r_max, kernel):
         "from paper_1702_00817_b200 import batch\n"
         "x = torch.from_numpy(np.load(sys.argv[1])).cuda()\n"
         f"s = batch.sweep_retain_sse(x, {r_min}, {r_max})\n"
-        "np.save(sys.argv[2], s.cpu().numpy())\n"
+        f"s2, sf = batch.sweep_retain_sse_unrounded(x, {r_min}, {r_max})\n"
+        "assert torch.equal(s, s2)\n"
+        "np.save(sys.argv[2], np.stack([s.cpu().numpy(), sf.cpu().numpy()]))\n"
     )
     import tempfile
 
@@ -201,7 +203,9 @@ def test_sweep_shapes_and_ranges(cuda, shape, r_min, r_max, kernel):
                            env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-3000:]
         got = np.load(os.path.join(td, "s.npy"))
-    assert np.array_equal(got, want)
+    assert np.array_equal(got[0], want)
+    want_f = np.stack([exact.compress_retain(x.numpy(), r)[2] for r in range(r_min, r_max + 1)], axis=1)
+    assert np.array_equal(got[1], want_f)
 
 
 def test_sweep_matches_oracle(cuda):
