@@ -87,6 +87,11 @@ typedef struct adct_qtab {
   int32_t max_abs_v;    /* proven bound of |64*(x_hat-128)| before clamping */
   int32_t quality;      /* JPEG quality used to build it, or -1 for an explicit table */
   int32_t aligned;      /* 1: max_abs_v + 32 <= 24575: fused one-op output clamp, no bit flip */
+  /* Float quantiser (default device path): q = RN(1.5*2^23 + Z * r) - 1.5*2^23
+   * in fp32 (one FFMA2 per lane pair), r = the float bits below, chosen just
+   * above 1/Q' so exact ties round away from zero; verified exhaustively over
+   * |Z| <= 8192 like the integer constants above. */
+  uint32_t recip_f[64];
 } adct_qtab_t;
 
 /* Build from an unrounded Q' table (64 float64, row-major), i.e. the output of

@@ -41,6 +41,7 @@ class QTab(ctypes.Structure):
         ("max_abs_v", c_int32),
         ("quality", c_int32),
         ("aligned", c_int32),
+        ("recip_f", ctypes.c_uint32 * 64),
     ]
 
 

@@ -68,6 +68,48 @@ __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
   return (qa + (qb << 16)) * c.w + TAB::wadd(q, p);
 }
 
+// Float quantiser (QF kernels): both lanes at once on the FP32x2 pipe.
+// `zb` is the linear form biased by 0x80008000, i.e. two unsigned 16-bit
+// fields Z + 32768 (|Z| <= 8192, no borrow).  PRMT places each field under
+// the exponent of 2^23, so the two floats are 2^23 + 32768 + Z exactly; one
+// FADD2 removes the offset (exact), one FFMA2 computes RN(M + Z r) with
+// M = 1.5 * 2^23 and r the float just above 1/Q' chosen by adct_qtab_build:
+// r - 1/Q' < 1/(2 Q' 8192) pushes exact ties away from zero and never moves a
+// non-tie across a rounding boundary, so the result is M + round_half_away(Z/Q')
+// (verified exhaustively over |Z| <= 8192 per position by the host).  The
+// result bits are 0x4B400000 + q; packing lanes with a shift and dequantising
+// with one IMAD leaves 0x4B400000 * qe in the product, which the host folds
+// into `wadd`.  Replaces SHF/LOP3 sign logic, the lane split and two
+// IMAD.HI per position (quant_pair below).
+constexpr float kQfMagic = 12582912.0f;                   // 1.5 * 2^23: ulp 1 over [2^23, 2^24)
+constexpr unsigned long long kQfOffset = 0x4B0080004B008000ull;  // (2^23 + 32768) in both halves
+constexpr u32 kQfBias = 0x80008000u;                      // +32768 in both 16-bit fields
+
+// The magic M as a run-time value (`small` is a kernel parameter < 256, so the
+// add is 0): ptxas cannot fold it, keeps it in one register and gives FFMA2's
+// immediate slot to r (otherwise every position's r costs a MOV).
+__device__ __forceinline__ float qf_magic(int32_t small) { return __uint_as_float(0x4B400000u + ((u32)small >> 8)); }
+
+__device__ __forceinline__ void quant_lanes_f(u32 zb, float r, u32& qa, u32& qb, float magic) {
+  const u32 fa = __byte_perm(zb, 0x4B000000u, 0x7610);  // 2^23 + field A
+  const u32 fb = __byte_perm(zb, 0x4B000000u, 0x7632);  // 2^23 + field B
+  unsigned long long F, Zf, Q, R, Mm;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(F) : "r"(fa), "r"(fb));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(R) : "f"(r));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(Mm) : "f"(magic));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(Zf) : "l"(F), "l"(kQfOffset));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(Q) : "l"(Zf), "l"(R), "l"(Mm));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(qa), "=r"(qb) : "l"(Q));
+}
+
+template <class TAB = ParamTab>
+__device__ __forceinline__ u32 quant_pair_f(u32 zb, int p, const QParamsDev& q, float magic) {
+  const uint4 c = TAB::pos(q, p);  // x: r (float bits), w: qe
+  u32 qa, qb;
+  quant_lanes_f(zb, __uint_as_float(c.x), qa, qb, magic);
+  return (qa + (qb << 16)) * c.w + TAB::wadd(q, p);
+}
+
 // ---------------------------------------------------------------------------
 // K2: fused retain-r, r a template parameter (pruned at compile time).
 // ---------------------------------------------------------------------------
@@ -257,11 +299,12 @@ __device__ __forceinline__ void cp_async_rows(uint4* slot_base, const TileCursor
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-template <bool PAIR, bool FLIP, class TAB = ParamTab>
+template <bool PAIR, bool FLIP, class TAB = ParamTab, bool QF = false>
 __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
   extern __shared__ uint4 s_ring[];  // [2][8][kThreads]
+  const float magic = qf_magic(ps.n_planes);
   const int64_t stride = gridDim.x;
   int64_t tile = blockIdx.x;
   if (tile >= n_tiles) return;
@@ -298,9 +341,14 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
 #pragma unroll
         for (int i = 0; i < 8; ++i) col[i] = t[i][v];
         fwd8(col, Zc);
+        if (QF) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) Zc[u] += kQfBias;  // folds into the butterfly's last IADD3
+        }
         if (v == 0) Zc[0] -= 8192u * 65537u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) Wc[u] = quant_pair<TAB>(Zc[u], u * 8 + v, q);
+        for (int u = 0; u < 8; ++u)
+          Wc[u] = QF ? quant_pair_f<TAB>(Zc[u], u * 8 + v, q, magic) : quant_pair<TAB>(Zc[u], u * 8 + v, q);
         inv8(Wc, cc);
 #pragma unroll
         for (int i = 0; i < 8; ++i) c[i][v] = cc[i];
@@ -340,12 +388,13 @@ __device__ __forceinline__ u32 pack_px8(const int (&V)[8], int half) {
 
 constexpr unsigned long long kHybridSmem = 64ull * kThreads * sizeof(int) + 8ull * kThreads * sizeof(uint4);
 
-template <class TAB = ParamTab>
+template <class TAB = ParamTab, bool QF = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_quant_hybrid(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
   extern __shared__ uint4 s_dyn[];
   uint4* s_orig = s_dyn;                                          // [8][kThreads]
   int* s_wb = reinterpret_cast<int*>(s_dyn + 8 * kThreads);       // [64][kThreads]
+  const float magic = qf_magic(ps.n_planes);
   UnitLoc L;
   u32 acc = 0;
   if (locate_unit<true>(ps, L)) {
@@ -367,16 +416,25 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int i = 0; i < 8; ++i) col[i] = t[i][v];
         fwd8(col, Zc);
+        if (QF) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) Zc[u] += kQfBias;
+        }
         if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int p = u * 8 + v;
           const uint4 c = TAB::pos(q, p);
           const u32 z = Zc[u];
-          const u32 sg = (TAB::kBaked && c.y == 2u) ? 0u : ((z >> 15) & 0x10001u) ^ 0x10001u;
-          const u32 U = z * c.y + c.z + sg;
-          const u32 qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
-          const u32 qb = __umulhi(U >> 16, c.x);      // lane B
+          u32 qa, qb;
+          if (QF) {
+            quant_lanes_f(z, __uint_as_float(c.x), qa, qb, magic);  // 0x4B400000 + q per lane
+          } else {
+            const u32 sg = (TAB::kBaked && c.y == 2u) ? 0u : ((z >> 15) & 0x10001u) ^ 0x10001u;
+            const u32 U = z * c.y + c.z + sg;
+            qa = __umulhi(U & 0xFFFFu, c.x);  // q + kq, lane A
+            qb = __umulhi(U >> 16, c.x);      // lane B
+          }
           wa[u] = (int)(qa * c.w) + (int)TAB::wadd(q, p);
           s_wb[p * kThreads + threadIdx.x] = (int)(qb * c.w) + (int)TAB::wadd(q, p);
         }

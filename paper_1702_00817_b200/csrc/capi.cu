@@ -188,6 +188,31 @@ bool to_qparams_hybrid(const adct_qtab_t& t, QParamsDev* q) {
   return true;
 }
 
+// Float-quantiser constants (QF kernels): pos.x = r (float bits), pos.w = qe;
+// the packed result carries 0x4B400000 + q per lane, whose 0x4B400000 * qe
+// is cancelled in wadd.  `scalar`: hybrid kernel offsets (no lane replication).
+QParamsDev to_qparams_f(const adct_qtab_t& t, bool scalar) {
+  QParamsDev q;
+  std::memset(&q, 0, sizeof q);
+  const uint32_t dc_out = t.aligned ? 24576u : 32768u;
+  for (int p = 0; p < 64; ++p) {
+    q.pos[p].x = t.recip_f[p];
+    q.pos[p].w = (uint32_t)t.qe[p];
+    q.wadd[p] = (uint32_t)0 - 0x4B400000u * (uint32_t)t.qe[p];
+  }
+  q.wadd[0] += scalar ? 32u + 8192u : (dc_out + 32u) * 65537u;
+  return q;
+}
+
+// ADCT_QUANT_FLOAT = 0 selects the integer (multiply-high) quantiser (A/B).
+int quant_float_choice() {
+  static const int v = [] {
+    const char* e = std::getenv("ADCT_QUANT_FLOAT");
+    return (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }();
+  return v;
+}
+
 // ADCT_WIDE_KERNEL = scalar forces k_quant_wide for every coarse table (A/B).
 int wide_kernel_choice() {
   static const int v = [] {
@@ -225,6 +250,36 @@ inline double ref_d(int u) {
 inline int64_t rha_div(int64_t z, int64_t q) {
   const int64_t a = (2 * (z < 0 ? -z : z) + q) / (2 * q);
   return z < 0 ? -a : a;
+}
+
+// Float quantiser constant: the float r just above 1/Q such that
+// RN(M + Z r) - M == round_half_away(Z / Q) for every |Z| <= zmax, M = 1.5 * 2^23
+// (the device FFMA2 computes M + Z r exactly and rounds once, ties to even).
+// Verified in exact integer arithmetic: r = mant * 2^-sh, so M + Z r rounds to
+// M + round_half_even(Z mant / 2^sh) (M is even).
+bool float_recip(int64_t Q, int64_t zmax, uint32_t* bits) {
+  float r = (float)(1.0 / (double)Q);
+  for (int attempt = 0; attempt < 64; ++attempt, r = std::nextafter(r, 2.0f)) {
+    int e = 0;
+    const float fr = std::frexp(r, &e);  // r = fr * 2^e, fr in [0.5, 1)
+    const int64_t mant = (int64_t)std::ldexp((double)fr, 24);  // exact 24-bit integer
+    const int sh = 24 - e;  // r = mant * 2^-sh
+    if (sh < 1 || sh > 62) return false;
+    // r must exceed 1/Q strictly (mant * Q > 2^sh) and by less than 1/(2 Q zmax)
+    bool ok = true;
+    for (int64_t Z = -zmax; ok && Z <= zmax; ++Z) {
+      const int64_t num = Z * mant;
+      int64_t fl = num >> sh;  // floor (arithmetic shift)
+      const int64_t rem = num - (fl << sh), half = (int64_t)1 << (sh - 1);
+      if (rem > half || (rem == half && (fl & 1))) ++fl;
+      if (fl != rha_div(Z, Q)) ok = false;
+    }
+    if (ok) {
+      std::memcpy(bits, &r, sizeof r);
+      return true;
+    }
+  }
+  return false;
 }
 
 int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out) {
@@ -279,6 +334,8 @@ int build_qtab_from_rounded(const int32_t* qp, int32_t quality, adct_qtab_t* out
     } else {
       packed_ok = false;
     }
+
+    if (!float_recip(Q, kZmax, &out->recip_f[p])) return ADCT_ERR_UNSUPPORTED;
 
     // Scalar quantiser: U = 2Z - [Z<0] + C, C = Q'(2K+1), divisor 2Q'.
     {
@@ -519,7 +576,9 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
   for (int p = 0; p < 64; ++p)
     if (qtab->qprime[p] < 1) return ADCT_ERR_NON_POSITIVE_QUANTIZER;
   if (!qtab->wide && qtab->mult[0] == 0) return ADCT_ERR_INVALID_ARGUMENT;  // not built by adct_qtab_*
-  const bool wide = qtab->wide != 0;
+  // float quantiser: any Q' fits, so only the inverse's range decides "wide"
+  const bool qf = quant_float_choice() == 1 && qtab->recip_f[0] != 0u;
+  const bool wide = (qf && quant_kernel_choice() == 1) ? (qtab->max_abs_v + 32 > 32767) : qtab->wide != 0;
   PlaneSetHost ps;
   int rc = build_planes(planes, n_planes, n_frames, ps, wide);
   if (rc != ADCT_OK) return rc;
@@ -529,18 +588,25 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
   u64* d_sse = reinterpret_cast<u64*>(sse);
   if (wide) {
     QParamsDev qh;
-    if (wide_kernel_choice() == 1 && to_qparams_hybrid(*qtab, &qh)) {
+    if (wide_kernel_choice() == 1 && (qf ? (qh = to_qparams_f(*qtab, true), true) : to_qparams_hybrid(*qtab, &qh))) {
       PlaneSetHost ph;  // two blocks per thread where every plane pairs
       rc = build_planes(planes, n_planes, n_frames, ph, false);
       if (rc != ADCT_OK) return rc;
       if (ph.pair) {
-        if (void* jf = jit::quant_function(jit::kHybrid, qh, s)) {  // table-specialised build
+        if (void* jf = jit::quant_function(qf ? jit::kHybridF : jit::kHybrid, qh, s)) {  // table-specialised build
           void* args[] = {&ph.dev, &qh, &d_sse};
           int rcj = ADCT_OK;
           const int rcc = for_frame_chunks(ph, n_frames, [&](dim3 g) {
             if (jit::launch(jf, g, dim3(kThreads), kHybridSmem, s, args) != 0) rcj = ADCT_ERR_CUDA;
           });
           return rcj != ADCT_OK ? rcj : rcc;
+        }
+        if (qf) {
+          ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid<ParamTab, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHybridSmem));
+          return for_frame_chunks(ph, n_frames, [&](dim3 g) {
+            k_quant_hybrid<ParamTab, true><<<g, kThreads, kHybridSmem, s>>>(ph.dev, qh, d_sse);
+          });
         }
         ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_hybrid<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kHybridSmem));
@@ -552,7 +618,8 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     const QParamsWide qw = to_qparams_wide(*qtab);
     return for_frame_chunks(ps, n_frames, [&](dim3 g) { k_quant_wide<<<g, kThreads, 0, s>>>(ps.dev, qw, d_sse); });
   }
-  const QParamsDev q = to_qparams(*qtab);
+  // the one-tile-per-CTA A/B kernel (ADCT_QUANT_KERNEL=grid) keeps the integer quantiser
+  const QParamsDev q = (qf && quant_kernel_choice() == 1) ? to_qparams_f(*qtab, false) : to_qparams(*qtab);
   const bool al = qtab->aligned != 0;
   if (quant_kernel_choice() == 1 && ps.grid_x > 0 && n_frames > 0) {
     const int64_t n_tiles = (int64_t)ps.grid_x * n_frames;
@@ -562,8 +629,9 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     if ((int64_t)grid > n_tiles) grid = (int)n_tiles;
     ps.dev.frame_base = 0;
     const size_t smem = 2 * 8 * kThreads * sizeof(uint4);
-    const int kind = ps.pair ? (al ? jit::kQuantPairAligned : jit::kQuantPairFlip)
-                             : (al ? jit::kQuantSingleAligned : jit::kQuantSingleFlip);
+    const int kind = (ps.pair ? (al ? jit::kQuantPairAligned : jit::kQuantPairFlip)
+                              : (al ? jit::kQuantSingleAligned : jit::kQuantSingleFlip)) +
+                     (qf ? jit::kFloatOffset : 0);
     if (void* jf = jit::quant_function(kind, q, s)) {  // table-specialised build
       QParamsDev qa = q;
       uint32_t tpf = ps.grid_x;
@@ -571,16 +639,22 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
       if (jit::launch(jf, dim3(grid), dim3(kThreads), smem, s, args) != 0) return ADCT_ERR_CUDA;
       return ADCT_OK;
     }
-#define ADCT_QP(PA, FL)                                                                        \
-  do {                                                                                         \
-    ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL>,                                      \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_quant_p<PA, FL><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x);      \
+#define ADCT_QP(PA, FL, QF)                                                                    \
+  do {                                                                                             \
+    ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_p<PA, FL, ParamTab, QF>,                            \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));     \
+    k_quant_p<PA, FL, ParamTab, QF><<<grid, kThreads, smem, s>>>(ps.dev, q, d_sse, n_tiles, ps.grid_x); \
   } while (0)
-    if (ps.pair) {
-      if (al) ADCT_QP(true, false); else ADCT_QP(true, true);
+    if (qf) {
+      if (ps.pair) {
+        if (al) ADCT_QP(true, false, true); else ADCT_QP(true, true, true);
+      } else {
+        if (al) ADCT_QP(false, false, true); else ADCT_QP(false, true, true);
+      }
+    } else if (ps.pair) {
+      if (al) ADCT_QP(true, false, false); else ADCT_QP(true, true, false);
     } else {
-      if (al) ADCT_QP(false, false); else ADCT_QP(false, true);
+      if (al) ADCT_QP(false, false, false); else ADCT_QP(false, true, false);
     }
 #undef ADCT_QP
     ADCT_CUDA_TRY(cudaGetLastError());

@@ -41,8 +41,8 @@ def test_prototypes_cover_header_exactly():
 
 
 def test_struct_sizes_match_header():
-    # adct_qtab_t: 10 x 64 int32 + 4 int32; adct_plane_t: 2 ptr + 2 int32 + 2 int64
-    assert ctypes.sizeof(_lib.QTab) == (10 * 64 + 4) * 4
+    # adct_qtab_t: 10 x 64 int32 + 4 int32 + 64 uint32 (recip_f); adct_plane_t: 2 ptr + 2 int32 + 2 int64
+    assert ctypes.sizeof(_lib.QTab) == (11 * 64 + 4) * 4
     assert ctypes.sizeof(_lib.Plane) == 8 + 8 + 4 + 4 + 8 + 8
 
 
@@ -128,6 +128,46 @@ def test_qtab_scalar_quantiser_constants_are_exact():
         assert U.min() >= 0 and U.max() < 2**32
         got = ((U.astype(np.uint64) * mag[:, None]) >> np.uint64(32)).astype(np.int64) - kw[:, None]
         assert np.array_equal(got, want)
+
+
+def _float_quantiser_replay(t):
+    """RN(M + Z r) - M for every |Z| <= 8192 and position, in exact integer
+    arithmetic (what the device FFMA2 computes: exact product, one rounding to
+    the ulp-1 grid of [2^23, 2^24), ties to even; M = 1.5 * 2^23 is even)."""
+    bits = np.frombuffer(bytes(t.recip_f), dtype=np.uint32)
+    r = bits.view(np.float32).astype(np.float64)
+    mant, e = np.frexp(r)  # r = mant * 2^e, mant in [0.5, 1)
+    m24 = np.ldexp(mant, 24).astype(np.int64)  # exact 24-bit integer
+    sh = (24 - e).astype(np.int64)
+    Z = np.arange(-8192, 8193, dtype=np.int64)
+    num = Z[None, :] * m24[:, None]
+    fl = num >> sh[:, None]
+    rem = num - (fl << sh[:, None])
+    half = np.left_shift(np.int64(1), sh - 1)[:, None]
+    return fl + ((rem > half) | ((rem == half) & (fl & 1 == 1))), Z
+
+
+def test_qtab_float_quantiser_is_exact():
+    """The float quantiser constants (recip_f, the default device path) give
+    round-half-away-from-zero of Z / Q' for every reachable Z, across quality
+    tables and explicit Q' over the whole supported range."""
+    rng = np.random.default_rng(5)
+    tables = [quant.quant_table(q) for q in (1, 5, 10, 25, 50, 75, 90, 100)]
+    grid = np.unique(np.concatenate([np.arange(1, 600), np.geomspace(600, 2**20, 60).round(),
+                                     2.0 ** np.arange(21), 2.0 ** np.arange(1, 21) + 1, 3 * 2.0 ** np.arange(19),
+                                     rng.integers(1, 20000, 256)]))
+    grid = grid[grid <= 2**20]
+    for k in range(0, len(grid), 64):
+        chunk = np.resize(grid[k:k + 64], 64).astype(np.float64)
+        tables.append(quant.quant_table(qprime_unrounded=chunk.reshape(8, 8)))
+    for t in tables:
+        got, Z = _float_quantiser_replay(t)
+        Qp = quant.qtab_qprime(t).reshape(64)
+        want = np.sign(Z)[None, :] * ((2 * np.abs(Z)[None, :] + Qp[:, None]) // (2 * Qp[:, None]))
+        assert np.array_equal(got, want)
+        # r is within 2^-13 relative of 1/Q' (the exhaustive replay above is the property)
+        r = np.frombuffer(bytes(t.recip_f), dtype=np.uint32).view(np.float32).astype(np.float64)
+        assert np.all(np.abs(r * Qp - 1.0) < 2.0 ** -13)
 
 
 def test_qtab_build_from_fold_and_errors():
