@@ -212,3 +212,65 @@ def test_zigzag_matches_reference(reference):
     from paper_1702_00817_b200 import codec
 
     assert tuple(reference.codec.ZIGZAG_INDICES) == codec.ZIGZAG_INDICES == exact.zigzag_indices()
+
+
+# --- the plain-C oracle (oracle/exact_c.c via oracle/fast.py): pinned to the
+# --- reference-made golden vectors and to the numpy oracle --------------------------
+
+def test_c_oracle_config0_golden():
+    from oracle import fast
+
+    g = GOLDEN["config0"]
+    Z = fast.forward(IMAGES["c0_seed0_512"])[0].astype(np.int64)
+    assert sha(Z) == g["coef_sha256_int64"]
+    assert np.array_equal(fast.forward(IMAGES["noise_64"], level_shift=True),
+                          exact.forward_unscaled(IMAGES["noise_64"], level_shift=True)[None])
+
+
+@pytest.mark.parametrize("name", ["c0_seed0_512", "c1_seed1_128", "c1_seed2_128", "ragged_40x24", "noise_64", "saturated_32x48"])
+def test_c_oracle_retain_golden(name):
+    from oracle import fast
+
+    img = IMAGES[name]
+    for r_s, g in GOLDEN["config1"][name].items():
+        rec, sse, ssef = fast.compress_retain(img, int(r_s), threads=3)
+        assert int(sse[0]) == g["sse_rounded"] and sha(rec[0]) == g["rec_sha256"], (name, r_s)
+        assert ssef[0] / (4096.0 * img.size) == pytest.approx(g["mse_ref"], rel=1e-9, abs=1e-12)
+
+
+def test_c_oracle_sweep_golden_and_numpy():
+    from oracle import fast
+
+    name = "c1_seed1_128"
+    s, sf = fast.sweep_sse(IMAGES[name], 1, 45, threads=2)
+    assert [int(v) for v in s[0]] == [GOLDEN["config1"][name][str(r)]["sse_rounded"] for r in range(1, 46)]
+    img = np.stack([IMAGES["c1_seed1_128"], IMAGES["c1_seed2_128"]])
+    s, sf = fast.sweep_sse(img, 3, 17)
+    assert np.array_equal(s, exact.sweep_sse(img, 3, 17))
+    assert np.array_equal(sf[:, 10 - 3], exact.compress_retain(img, 10)[2])
+
+
+@pytest.mark.parametrize("name", ["c2_seed3_128", "noise_64", "saturated_32x48", "ragged_40x24"])
+@pytest.mark.parametrize("q", [10, 50, 75, 90])
+def test_c_oracle_quant_golden(name, q):
+    from oracle import fast
+    from paper_1702_00817_b200.quant import q50_luma
+
+    g = GOLDEN["quant"][name][str(q)]
+    rec, sse = fast.compress_quant(IMAGES[name], exact.qprime(q50_luma(), q), threads=4)
+    assert int(sse[0]) == g["sse"] and sha(rec[0]) == g["rec_sha256"]
+
+
+def test_c_oracle_equals_numpy_oracle_random():
+    """Random batches, ragged shapes, extreme tables: the two oracles agree."""
+    from oracle import fast
+
+    rng = np.random.default_rng(11)
+    for shape in ((3, 64, 96), (2, 40, 24), (1, 8, 8)):
+        x = rng.integers(0, 256, shape, dtype=np.uint8)
+        for Qp in (np.ones((8, 8), np.int64), rng.integers(1, 3000, (8, 8)), np.full((8, 8), 2**20)):
+            a, b = exact.compress_quant(x, Qp), fast.compress_quant(x, Qp, threads=3)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        for r in (1, 2, 10, 33, 64):
+            a, b = exact.compress_retain(x, r), fast.compress_retain(x, r, threads=2)
+            assert all(np.array_equal(u, v) for u, v in zip(a, b)), r
