@@ -27,7 +27,9 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    ref_installed = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "adct"))
+    assert d["cpu_baseline"]["kind"] == ("reference" if ref_installed else "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["units_per_gpu"] == 1 and d["config"]["pixels_per_step"] == 512 * 512
 
 
 def test_reference_arm_nonzero_rank_is_silent():
@@ -35,3 +37,38 @@ def test_reference_arm_nonzero_rank_is_silent():
                         "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, RANK="1"))
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def _plan(nproc, *extra):
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+           "--gpus", str(nproc), "--plan", *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=dict(os.environ, ADCT_DIST_BACKEND="gloo"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_two_rank_plan_is_strong_scaling_of_config3():
+    """torchrun --nproc-per-node 2 bench.py --gpus 2: BASELINE config 3's 4096
+    images split over the ranks (not 4096 per rank)."""
+    d = _plan(2)
+    assert d["config"]["units_per_gpu"] == 2048
+    assert d["config"]["pixels_per_step"] == 17179869184  # 4096 x 2048^2, the whole config once
+    assert d["config"]["scaling"] == "strong" and d["units_all_ranks"] == 4096
+    assert d["first_unit_per_rank"] == [0, 2048]
+
+
+def test_two_rank_plan_config4_frames_and_weak_option():
+    d = _plan(2, "--config", "4")
+    assert d["config"]["units_per_gpu"] == 256 and d["units_all_ranks"] == 512
+    assert d["config"]["pixels_per_step"] == 512 * (3840 * 2160 + 2 * 1920 * 1080)
+    w = _plan(2, "--scaling", "weak")
+    assert w["config"]["units_per_gpu"] == 4096 and w["config"]["pixels_per_step"] == 2 * 17179869184
