@@ -66,6 +66,15 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_OUT = None  # the real stdout (main() points fd 1 at stderr)
+
+
+def emit(line: dict) -> None:
+    out = _OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def measured_hbm_peak() -> tuple[float, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -373,7 +382,7 @@ def reference_arm(args) -> None:
                          "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def config_block(config: int, world: int, scaling: str, p: dict, fused: bool = False) -> dict:
@@ -706,7 +715,7 @@ def gpu_arm(args) -> None:
         }
         if secondary:
             line["secondary"] = secondary
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
@@ -731,11 +740,12 @@ def plan_arm(args) -> None:
     else:
         units, firsts = p["per"], [p["first"]]
     if rank == 0:
-        print(json.dumps({"plan": p, "units_all_ranks": units, "first_unit_per_rank": firsts,
-                          "config": config_block(args.config, world, args.scaling, p)}), flush=True)
+        emit({"plan": p, "units_all_ranks": units, "first_unit_per_rank": firsts,
+              "config": config_block(args.config, world, args.scaling, p)})
 
 
 def main() -> None:
+    global _OUT
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -757,6 +767,12 @@ def main() -> None:
     ap.add_argument("--e2e-images", type=int, default=256)
     ap.add_argument("--e2e-chunk-mb", type=int, default=32)
     args = ap.parse_args()
+    # stdout carries exactly one JSON line: anything else the libraries print
+    # to fd 1 (e.g. NCCL's "NCCL version ..." banner when symmetric memory
+    # initialises it) is sent to stderr, and the JSON goes to a saved copy of fd 1
+    _OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
