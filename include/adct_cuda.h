@@ -258,9 +258,13 @@ int adct_synth_blobs(uint8_t* out, int64_t n, int32_t h, int32_t w,
  * corpus.py:65-111, each through compress_image + mse, cli.py:101-113) for
  * whole batches: H2D copy of chunk i+1, fused compress of chunk i and D2H
  * copy of chunk i-1 overlap on separate streams.
- * Host buffers should be pinned for full speed: adct_host_alloc memory
- * (cudaHostAlloc) reaches the PCIe limit; adct_host_register'd memory runs
- * ~9 % slower on the B200 boxes measured (tools/pcie_probe2.py).
+ * Host buffers may be ordinary pageable memory (e.g. numpy arrays): the
+ * pipeline then stages every chunk through its own page-locked ring (host
+ * threads fill and drain it while the previous chunks' copies and kernels
+ * run; nothing is registered per call; ADCT_PIPELINE_THREADS sets the
+ * thread count).  Page-locked buffers (adct_host_alloc, cudaHostAlloc, or
+ * adct_host_register'd) skip the staging and are copied directly — the
+ * fastest case.  Errors drain every pipeline stream before returning.
  * ------------------------------------------------------------------------- */
 typedef struct adct_pipeline adct_pipeline_t;
 
@@ -288,6 +292,8 @@ int adct_quant_jit_stats(int64_t* compiled, int64_t* launches, int64_t* failures
 /* Page-lock / unlock caller memory (cudaHostRegister). */
 int adct_host_register(void* ptr, size_t bytes);
 int adct_host_unregister(void* ptr);
+/* 1 if ptr is page-locked host memory (cudaHostAlloc'ed or registered), else 0. */
+int adct_host_is_pinned(const void* ptr);
 /* Page-locked host allocation (cudaHostAlloc, portable); *out = NULL for 0 bytes. */
 int adct_host_alloc(size_t bytes, void** out);
 int adct_host_free(void* ptr);

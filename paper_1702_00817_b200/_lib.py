@@ -116,6 +116,7 @@ PROTOTYPES = {
     ),
     "adct_host_register": (c_int, [c_void_p, c_size_t]),
     "adct_host_unregister": (c_int, [c_void_p]),
+    "adct_host_is_pinned": (c_int, [c_void_p]),
     "adct_pipeline_compress_quant_planes": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]),
     "adct_quant_jit_stats": (c_int, [POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "adct_host_alloc": (c_int, [c_size_t, POINTER(c_void_p)]),

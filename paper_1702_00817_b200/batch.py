@@ -10,6 +10,7 @@ libadct_cuda.so.
 from __future__ import annotations
 
 import ctypes
+import functools
 from typing import Sequence
 
 import numpy as np
@@ -20,7 +21,51 @@ from .errors import BadDimensions, DimensionMismatch, InvalidRetention
 
 
 def _stream() -> int:
+    # the current stream of the current device, which _device_guard has set
+    # to the device of the call's tensors
     return torch.cuda.current_stream().cuda_stream
+
+
+def _device_guard(fn):
+    """Run `fn` with its tensors' CUDA device current: the C ABI launches on
+    the current device and the stream passed in, so a tensor on another GPU
+    must not be launched in this device's context or on its stream."""
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        dev = None
+        for a in (*args, *kwargs.values()):
+            if isinstance(a, (list, tuple)) and a:
+                a = a[0]
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                dev = a.device
+                break
+        if dev is None:
+            return fn(*args, **kwargs)
+        with torch.cuda.device(dev):
+            return fn(*args, **kwargs)
+
+    return wrapper
+
+
+def _check_out(out: torch.Tensor | None, images: torch.Tensor) -> None:
+    """`out` receives n frames of h x w bytes at its row/frame strides."""
+    if out is None:
+        return
+    n, h, w = images.shape
+    if (not isinstance(out, torch.Tensor) or out.dtype != torch.uint8 or out.device != images.device
+            or tuple(out.shape) != (n, h, w) or out.stride(2) != 1 or out.stride(1) != w
+            or (n > 1 and out.stride(0) < h * w)):
+        raise ValueError(f"out must be a uint8 ({n}, {h}, {w}) tensor with contiguous rows on {images.device}")
+
+
+def _check_vec(v: torch.Tensor | None, n: int, device, name: str = "sse_out") -> None:
+    """An int64 vector of n entries written at consecutive addresses."""
+    if v is None:
+        return
+    if (not isinstance(v, torch.Tensor) or v.dtype != torch.int64 or v.device != device or v.dim() != 1
+            or v.shape[0] != n or (n > 1 and v.stride(0) != 1)):
+        raise ValueError(f"{name} must be a contiguous int64 tensor of {n} entries on {device}")
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -51,6 +96,7 @@ def _img_stride(images: torch.Tensor) -> int:
     return images.stride(0) if n > 1 else h * w
 
 
+@_device_guard
 def forward_int(images: torch.Tensor, *, level_shift: bool = False, dtype=torch.int32,
                 out: torch.Tensor | None = None) -> torch.Tensor:
     """K1: T X T^T of every 8x8 block, (N, H*W/64, 8, 8) in `_tile` order (codec.py:74-81, 107-109).
@@ -70,6 +116,7 @@ def forward_int(images: torch.Tensor, *, level_shift: bool = False, dtype=torch.
     return out
 
 
+@_device_guard
 def compress_retain(
     images: torch.Tensor,
     r: int,
@@ -89,6 +136,8 @@ def compress_retain(
         raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
     images = _as_batch(images)
     n, h, w = images.shape
+    _check_out(out, images)
+    _check_vec(sse_out, n, images.device)
     rec = None
     if reconstruct:
         rec = out if out is not None else torch.empty_like(images)
@@ -102,6 +151,7 @@ def compress_retain(
     return rec, sse, ssef
 
 
+@_device_guard
 def compress_retain_exchange(
     images: torch.Tensor,
     r: int,
@@ -125,6 +175,8 @@ def compress_retain_exchange(
     n, h, w = images.shape
     if arrivals.dtype != torch.int32 or arrivals.numel() < n or arrivals.device != images.device:
         raise ValueError("arrivals must be an int32 tensor of >= N zeros on the images' device")
+    _check_out(out, images)
+    _check_vec(sse_out, n, images.device)
     rec = None
     if reconstruct:
         rec = out if out is not None else torch.empty_like(images)
@@ -137,6 +189,7 @@ def compress_retain_exchange(
     return rec, sse
 
 
+@_device_guard
 def compress_quant(
     images: torch.Tensor,
     qtab: _lib.QTab,
@@ -149,6 +202,8 @@ def compress_quant(
     inverse, +128, round, clamp.  Returns (rec | None, sse[N] int64)."""
     images = _as_batch(images)
     n, h, w = images.shape
+    _check_out(out, images)
+    _check_vec(sse_out, n, images.device)
     rec = (out if out is not None else torch.empty_like(images)) if reconstruct else None
     sse = sse_out if sse_out is not None else torch.empty(n, dtype=torch.int64, device=images.device)
     _lib.call(
@@ -174,6 +229,11 @@ def _planes(planes: Sequence[torch.Tensor], recs: Sequence[torch.Tensor | None])
         _, h, w = p.shape
         if h % 8 or w % 8:
             raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
+        if p.device != planes[0].device:
+            raise ValueError("every plane must be on the same device")
+        if r is not None and (not isinstance(r, torch.Tensor) or r.dtype != torch.uint8 or r.device != p.device
+                              or r.shape != p.shape or not r.is_contiguous()):
+            raise ValueError(f"plane {k}'s output must be a contiguous uint8 tensor shaped like the plane")
         arr[k].src = p.data_ptr()
         arr[k].dst = None if r is None else r.data_ptr()
         arr[k].height = h
@@ -183,6 +243,7 @@ def _planes(planes: Sequence[torch.Tensor], recs: Sequence[torch.Tensor | None])
     return arr, n
 
 
+@_device_guard
 def compress_quant_planes(planes: Sequence[torch.Tensor], qtab: _lib.QTab, *, reconstruct: bool = True):
     """K6: all planes (e.g. Y, Cb, Cr of 4:2:0 frames) in one launch.
     Returns (list of rec | None, sse (N, n_planes) int64)."""
@@ -193,6 +254,7 @@ def compress_quant_planes(planes: Sequence[torch.Tensor], qtab: _lib.QTab, *, re
     return recs, sse
 
 
+@_device_guard
 def compress_quant_planes_exchange(planes: Sequence[torch.Tensor], qtab: _lib.QTab, peers_dev: int, n_peers: int,
                                    peer_offset: int, arrivals: torch.Tensor, *, reconstruct: bool = True,
                                    out: Sequence[torch.Tensor] | None = None):
@@ -201,6 +263,8 @@ def compress_quant_planes_exchange(planes: Sequence[torch.Tensor], qtab: _lib.QT
     plane (see compress_retain_exchange).  `arrivals` is accepted for symmetry
     and left untouched.  Returns (recs, local sse (N, n_planes))."""
     recs = list(out) if out is not None else [torch.empty_like(p) if reconstruct else None for p in planes]
+    if len(recs) != len(planes):
+        raise ValueError("one output per plane")
     arr, n = _planes(planes, recs)
     if arrivals.dtype != torch.int32 or arrivals.numel() < n * len(planes) or arrivals.device != planes[0].device:
         raise ValueError("arrivals must be an int32 tensor of >= N * n_planes zeros on the planes' device")
@@ -210,6 +274,7 @@ def compress_quant_planes_exchange(planes: Sequence[torch.Tensor], qtab: _lib.QT
     return recs, sse
 
 
+@_device_guard
 def compress_retain_planes(planes: Sequence[torch.Tensor], r: int, *, reconstruct: bool = True):
     if not 1 <= int(r) <= 64:
         raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
@@ -220,6 +285,7 @@ def compress_retain_planes(planes: Sequence[torch.Tensor], r: int, *, reconstruc
     return recs, sse
 
 
+@_device_guard
 def sweep_retain_sse(images: torch.Tensor, r_min: int = 1, r_max: int = 45) -> torch.Tensor:
     """K7: SSE[N, r_max-r_min+1] for every r, one read of each image (cli.py:101-113)."""
     if not (1 <= r_min <= r_max <= 64):
@@ -232,6 +298,7 @@ def sweep_retain_sse(images: torch.Tensor, r_min: int = 1, r_max: int = 45) -> t
     return sse
 
 
+@_device_guard
 def sse_u8(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """Per-image integer SSE of two uint8 CUDA batches (N, ...) -> int64[N]."""
     if a.shape != b.shape:
@@ -245,6 +312,7 @@ def sse_u8(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return sse
 
 
+@_device_guard
 def forward_f64(images: torch.Tensor) -> torch.Tensor:
     """C X C^T per block in float64 (forward_2d / coefficient_blocks, codec.py:68-71, 120-131)."""
     if images.dim() == 2:
@@ -260,6 +328,7 @@ def forward_f64(images: torch.Tensor) -> torch.Tensor:
     return coef
 
 
+@_device_guard
 def inverse_f64(coef: torch.Tensor, h: int, w: int, *, r: int = 64, clamp: bool = False) -> torch.Tensor:
     """untile(C^T mask_r(Y) C), optionally clamped (inverse_2d / reconstruct_image)."""
     if not 1 <= int(r) <= 64:
@@ -306,6 +375,7 @@ def _f64_or_u8(images: torch.Tensor):
     return images.to(torch.float64).contiguous(), 1
 
 
+@_device_guard
 def forward_dense(images: torch.Tensor, C) -> torch.Tensor:
     """Y = C X C^T per block for any 8x8 C, float64 (coefficient_blocks, codec.py:120-131)."""
     x, f64 = _f64_or_u8(images)
@@ -315,6 +385,7 @@ def forward_dense(images: torch.Tensor, C) -> torch.Tensor:
     return coef
 
 
+@_device_guard
 def inverse_dense(coef: torch.Tensor, h: int, w: int, C, *, r: int = 64, clamp: bool = False) -> torch.Tensor:
     """untile(C^T mask_r(Y) C), optionally clamped (reconstruct_image, codec.py:134-141)."""
     if not 1 <= int(r) <= 64:
@@ -329,6 +400,7 @@ def inverse_dense(coef: torch.Tensor, h: int, w: int, C, *, r: int = 64, clamp: 
     return out
 
 
+@_device_guard
 def sweep_dense_sse(images: torch.Tensor, C, r_min: int, r_max: int) -> torch.Tensor:
     """float64 SSE[N, r] of the reference's unrounded, clamped reconstructions for any C."""
     if not (1 <= r_min <= r_max <= 64):
@@ -340,6 +412,7 @@ def sweep_dense_sse(images: torch.Tensor, C, r_min: int, r_max: int) -> torch.Te
     return sse
 
 
+@_device_guard
 def sweep_retain_sse_unrounded(images: torch.Tensor, r_min: int = 1, r_max: int = 45):
     """(rounded SSE, 4096 x unrounded SSE), both int64[N, r] — exact."""
     if not (1 <= r_min <= r_max <= 64):

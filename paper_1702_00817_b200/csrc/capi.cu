@@ -9,6 +9,8 @@
 #include <new>
 #include <vector>
 
+#include "host_copy.h"
+
 #include "adct_cuda.h"
 #define ADCT_DEFINE_PLAIN_KERNELS
 #include "adct_jit.h"
@@ -531,8 +533,10 @@ int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, i
   x.arrivals = arrivals;
   x.offset = peer_offset;
   x.n_peers = n_peers;
-  // packed CTA counting needs < 2^16 CTAs (128- or 256-unit tiles) per image
-  x.packed = ((int64_t)h / 8 * (w / 8) + 127) / 128 <= 65535 ? 1 : 0;
+  // packed CTA counting needs < 2^16 CTAs (128- or 256-unit tiles) per image;
+  // ADCT_XCHG_PACKED=0 forces the fenced arrival-counter form (tests)
+  const char* fp = std::getenv("ADCT_XCHG_PACKED");
+  x.packed = (fp && std::strcmp(fp, "0") == 0) ? 0 : (((int64_t)h / 8 * (w / 8) + 127) / 128 <= 65535 ? 1 : 0);
   adct_plane_t pl = single_plane(img, rec, h, w, img_stride, rec_stride);
   return retain_planes(&pl, 1, n, r, sse, nullptr, stream, &x);
 }
@@ -597,7 +601,10 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
           void* args[] = {&ph.dev, &qh, &d_sse};
           int rcj = ADCT_OK;
           const int rcc = for_frame_chunks(ph, n_frames, [&](dim3 g) {
-            if (jit::launch(jf, g, dim3(kThreads), kHybridSmem, s, args) != 0) rcj = ADCT_ERR_CUDA;
+            if (const int cr = jit::launch(jf, g, dim3(kThreads), kHybridSmem, s, args)) {
+              g_last_cuda = cr;  // CUresult of the driver launch
+              rcj = ADCT_ERR_CUDA;
+            }
           });
           return rcj != ADCT_OK ? rcj : rcc;
         }
@@ -636,7 +643,10 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
       QParamsDev qa = q;
       uint32_t tpf = ps.grid_x;
       void* args[] = {&ps.dev, &qa, &d_sse, const_cast<int64_t*>(&n_tiles), &tpf};
-      if (jit::launch(jf, dim3(grid), dim3(kThreads), smem, s, args) != 0) return ADCT_ERR_CUDA;
+      if (const int cr = jit::launch(jf, dim3(grid), dim3(kThreads), smem, s, args)) {
+        g_last_cuda = cr;  // CUresult of the driver launch
+        return ADCT_ERR_CUDA;
+      }
       return ADCT_OK;
     }
 #define ADCT_QP(PA, FL, QF)                                                                    \
@@ -903,27 +913,54 @@ struct adct_pipeline {
   static constexpr int kMaxDepth = 8;
   int depth = 3;  // streams / staging slots in flight (ADCT_PIPELINE_DEPTH, 2..8)
   cudaStream_t stream[kMaxDepth] = {};
+  cudaEvent_t done[kMaxDepth] = {};  // slot b's last chunk finished (staged path)
   uint8_t* d_in[kMaxDepth] = {};
   uint8_t* d_out[kMaxDepth] = {};
+  uint8_t* h_in[kMaxDepth] = {};   // page-locked staging ring for pageable callers
+  uint8_t* h_out[kMaxDepth] = {};
+  size_t h_bytes = 0;              // size of each h_in / h_out slot (0: not allocated yet)
   uint64_t* d_sse = nullptr;  // SSE of a whole call, copied to the host once at the end
   int64_t sse_cap = 0;
+  adct::HostCopyPool* pool = nullptr;  // host threads for the staging memcpys
 };
 
 namespace {
 
 void pipeline_free(adct_pipeline* p) {
   for (int k = 0; k < p->depth; ++k) {
+    if (p->stream[k]) cudaStreamSynchronize(p->stream[k]);
+  }
+  for (int k = 0; k < p->depth; ++k) {
     if (p->stream[k]) cudaStreamDestroy(p->stream[k]);
+    if (p->done[k]) cudaEventDestroy(p->done[k]);
     if (p->d_in[k]) cudaFree(p->d_in[k]);
     if (p->d_out[k]) cudaFree(p->d_out[k]);
+    if (p->h_in[k]) cudaFreeHost(p->h_in[k]);
+    if (p->h_out[k]) cudaFreeHost(p->h_out[k]);
   }
   if (p->d_sse) cudaFree(p->d_sse);
+  delete p->pool;
   delete p;
 }
 
+// Drain every stream before an error return: no copy may still be queued on
+// host or staging memory the caller is about to reuse or free.
+int pipeline_fail(adct_pipeline* p, int rc) {
+  for (int k = 0; k < p->depth; ++k)
+    if (p->stream[k]) cudaStreamSynchronize(p->stream[k]);
+  return rc;
+}
+
+#define ADCT_PIPE_TRY(expr)                                    \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return pipeline_fail(p, cuda_fail(_e)); \
+  } while (0)
+
 // Staging slots of at least `unit_bytes` (one image / one frame of planes)
-// and a device SSE vector of at least `n_sse` entries.
-int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse) {
+// and a device SSE vector of at least `n_sse` entries; with `staged`, also
+// the page-locked host ring of the same slot size.
+int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse, bool staged) {
   if (unit_bytes > p->chunk_bytes) {  // one unit larger than a chunk: grow the staging buffers
     for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
     const size_t nb = (unit_bytes + 15) / 16 * 16;
@@ -939,6 +976,22 @@ int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse) {
     }
     p->chunk_bytes = nb;
   }
+  if (staged && p->h_bytes < p->chunk_bytes) {  // page-locked ring, allocated on first pageable use
+    for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
+    p->h_bytes = 0;
+    for (int k = 0; k < p->depth; ++k) {
+      if (p->h_in[k]) ADCT_CUDA_TRY(cudaFreeHost(p->h_in[k]));
+      if (p->h_out[k]) ADCT_CUDA_TRY(cudaFreeHost(p->h_out[k]));
+      p->h_in[k] = p->h_out[k] = nullptr;
+    }
+    for (int k = 0; k < p->depth; ++k) {
+      ADCT_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->h_in[k]), p->chunk_bytes, cudaHostAllocPortable));
+      ADCT_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->h_out[k]), p->chunk_bytes, cudaHostAllocPortable));
+      if (p->done[k] == nullptr) ADCT_CUDA_TRY(cudaEventCreateWithFlags(&p->done[k], cudaEventDisableTiming));
+    }
+    p->h_bytes = p->chunk_bytes;
+    if (p->pool == nullptr) p->pool = new adct::HostCopyPool(adct::HostCopyPool::default_threads());
+  }
   if (n_sse > p->sse_cap) {  // grow the per-call device SSE vector
     if (p->d_sse) ADCT_CUDA_TRY(cudaFree(p->d_sse));
     p->d_sse = nullptr;
@@ -949,16 +1002,80 @@ int pipeline_reserve(adct_pipeline* p, size_t unit_bytes, int64_t n_sse) {
   return ADCT_OK;
 }
 
-// Frames of 1..3 host planes (e.g. 4:2:0 video): each chunk of frames is
-// gathered plane by plane (one 2-D copy per plane) into a frame-interleaved
-// staging slot [plane 0 | plane 1 | plane 2] per frame, compressed by the
-// one-launch planes kernel, and scattered back the same way.
-int pipeline_planes_run(adct_pipeline* p, const adct_plane_t* hp, int32_t n_planes, int64_t n_frames,
-                        const adct_qtab_t* qtab, uint64_t* host_sse) {
-  if (p == nullptr || hp == nullptr || qtab == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
+// Page-locked (cudaHostAlloc'ed or cudaHostRegister'ed) host memory?
+bool is_pinned(const void* ptr) {
+  if (ptr == nullptr) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// One chunk of host frames of 1..3 planes: how its bytes map between the
+// caller's arrays and a frame-interleaved slot [plane 0 | plane 1 | plane 2]
+// per frame (a single-image batch is one plane).
+struct ChunkMap {
+  const adct_plane_t* hp;
+  int n_planes;
+  size_t off[3];
+  size_t frame_bytes;
+};
+
+// Host segments (slot <- caller for inputs, caller <- slot for outputs) of frames [f0, f0+m).
+void chunk_segments(const ChunkMap& cm, int64_t f0, int64_t m, uint8_t* slot, bool out,
+                    std::vector<adct::HostCopyPool::Seg>& segs) {
+  segs.clear();
+  for (int k = 0; k < cm.n_planes; ++k) {
+    const adct_plane_t& q = cm.hp[k];
+    const size_t row = (size_t)q.height * q.width;
+    if (row == 0 || (out && q.dst == nullptr)) continue;
+    const int64_t fs = out ? q.dst_frame_stride : q.src_frame_stride;
+    if (cm.n_planes == 1 && (m == 1 || fs == (int64_t)row) && cm.frame_bytes == row) {
+      // contiguous frames map onto a contiguous slot: one segment
+      if (out) segs.push_back({q.dst + f0 * fs, slot, (size_t)m * row});
+      else segs.push_back({slot, q.src + f0 * fs, (size_t)m * row});
+      continue;
+    }
+    for (int64_t f = 0; f < m; ++f) {
+      uint8_t* s = slot + (size_t)f * cm.frame_bytes + cm.off[k];
+      if (out) segs.push_back({q.dst + (f0 + f) * fs, s, row});
+      else segs.push_back({s, q.src + (f0 + f) * fs, row});
+    }
+  }
+}
+
+// The compress launch of one chunk on the device slot.
+using ChunkLaunch = int (*)(const adct_plane_t* dev, int n_planes, int64_t m, int kind, int32_t r,
+                            const adct_qtab_t* qtab, uint64_t* sse, cudaStream_t s);
+
+int launch_chunk(const adct_plane_t* dev, int n_planes, int64_t m, int kind, int32_t r, const adct_qtab_t* qtab,
+                 uint64_t* sse, cudaStream_t s) {
+  if (kind == 0) {
+    if (n_planes == 1)  // single images: the retain entry point (128-unit pruned kernels)
+      return adct_compress_retain(dev[0].src, dev[0].dst, m, dev[0].height, dev[0].width, dev[0].src_frame_stride,
+                                  dev[0].dst_frame_stride, r, sse, nullptr, s);
+    return adct_compress_retain_planes(dev, n_planes, m, r, sse, s);
+  }
+  return adct_compress_quant_planes(dev, n_planes, m, qtab, sse, s);
+}
+
+// Frames of 1..3 host planes through the device in chunks of whole frames.
+// Pinned callers: each chunk is copied straight from/to their arrays (2-D
+// copies per plane), chunk i on stream i % depth so the copy engines overlap
+// chunk i's D2H with chunk i+1's H2D.  Pageable callers (ordinary numpy
+// arrays, never registered per call): the library's own page-locked ring is
+// filled and drained by host threads (HostCopyPool) while the previous
+// chunks' H2D / kernel / D2H run, one cudaMemcpyAsync per chunk each way.
+int pipeline_frames_run(adct_pipeline* p, const adct_plane_t* hp, int32_t n_planes, int64_t n_frames, int kind,
+                        int32_t r, const adct_qtab_t* qtab, uint64_t* host_sse) {
+  if (p == nullptr || hp == nullptr || n_planes < 1 || n_planes > 3 || n_frames < 0)
     return ADCT_ERR_INVALID_ARGUMENT;
-  size_t off[3] = {0, 0, 0}, frame_bytes = 0;
-  bool any_dst = false;
+  if (kind == 0 && (r < 1 || r > 64)) return ADCT_ERR_INVALID_RETENTION;
+  if (kind == 1 && qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  ChunkMap cm{hp, n_planes, {0, 0, 0}, 0};
+  bool any_dst = false, pinned = true;
   for (int k = 0; k < n_planes; ++k) {
     const adct_plane_t& q = hp[k];
     if (q.height < 0 || q.width < 0 || (q.height % 8) || (q.width % 8)) return ADCT_ERR_BAD_DIMENSIONS;
@@ -966,58 +1083,99 @@ int pipeline_planes_run(adct_pipeline* p, const adct_plane_t* hp, int32_t n_plan
     if (n_frames > 0 && px > 0 && q.src == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
     if (n_frames > 1 && (q.src_frame_stride < px || (q.dst && q.dst_frame_stride < px)))
       return ADCT_ERR_INVALID_ARGUMENT;
-    off[k] = frame_bytes;
-    frame_bytes += ((size_t)px + 15) / 16 * 16;
+    cm.off[k] = cm.frame_bytes;
+    cm.frame_bytes += n_planes == 1 ? (size_t)px : ((size_t)px + 15) / 16 * 16;
     any_dst = any_dst || q.dst != nullptr;
   }
   if (n_frames == 0) return ADCT_OK;
   if (host_sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
-  if (frame_bytes == 0) {
+  if (cm.frame_bytes == 0) {
     std::memset(host_sse, 0, (size_t)n_frames * n_planes * sizeof(uint64_t));
     return ADCT_OK;
   }
   ADCT_CUDA_TRY(cudaSetDevice(p->device));
-  int rc0 = pipeline_reserve(p, frame_bytes, n_frames * n_planes);
-  if (rc0 != ADCT_OK) return rc0;
-  const int64_t per = (int64_t)(p->chunk_bytes / frame_bytes);
-  int64_t chunk = 0;
-  for (int64_t f0 = 0; f0 < n_frames; f0 += per, ++chunk) {
-    const int b = (int)(chunk % p->depth);
-    const int64_t m = (n_frames - f0) < per ? (n_frames - f0) : per;
+  for (int k = 0; k < n_planes; ++k)
+    pinned = pinned && is_pinned(hp[k].src) && is_pinned(hp[k].dst);
+  const bool staged = !pinned;
+  int rc0 = pipeline_reserve(p, cm.frame_bytes, n_frames * n_planes, staged);
+  if (rc0 != ADCT_OK) return pipeline_fail(p, rc0);
+  const int64_t per = (int64_t)(p->chunk_bytes / cm.frame_bytes);
+  const int64_t n_chunks = (n_frames + per - 1) / per;
+  std::vector<adct::HostCopyPool::Seg> segs;
+  auto chunk_frames = [&](int64_t c) { return std::min<int64_t>(per, n_frames - c * per); };
+  std::vector<adct::HostCopyPool::Seg> segs_out;
+  // staged path: results of chunk c leave the ring once its slot's event
+  // fired; their segments join the next input fill in one pool batch
+  auto drain = [&](int64_t c, bool run_now) -> int {
+    const int b = (int)(c % p->depth);
+    ADCT_PIPE_TRY(cudaEventSynchronize(p->done[b]));
+    segs_out.clear();
+    if (any_dst) chunk_segments(cm, c * per, chunk_frames(c), p->h_out[b], true, segs_out);
+    if (run_now) p->pool->run(segs_out);
+    return ADCT_OK;
+  };
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int b = (int)(c % p->depth);
+    const int64_t f0 = c * per, m = chunk_frames(c);
     cudaStream_t s = p->stream[b];
     adct_plane_t dev[3];
     for (int k = 0; k < n_planes; ++k) {
-      const adct_plane_t& q = hp[k];
-      const size_t row = (size_t)q.height * q.width;
-      const size_t sfs = m > 1 ? (size_t)q.src_frame_stride : row;
-      if (row)
-        ADCT_CUDA_TRY(cudaMemcpy2DAsync(p->d_in[b] + off[k], frame_bytes, q.src + f0 * q.src_frame_stride, sfs,
-                                        row, (size_t)m, cudaMemcpyHostToDevice, s));
-      dev[k].src = p->d_in[b] + off[k];
-      dev[k].dst = any_dst ? p->d_out[b] + off[k] : nullptr;
-      dev[k].height = q.height;
-      dev[k].width = q.width;
-      dev[k].src_frame_stride = (int64_t)frame_bytes;
-      dev[k].dst_frame_stride = (int64_t)frame_bytes;
+      dev[k].src = p->d_in[b] + cm.off[k];
+      dev[k].dst = any_dst ? p->d_out[b] + cm.off[k] : nullptr;
+      dev[k].height = hp[k].height;
+      dev[k].width = hp[k].width;
+      dev[k].src_frame_stride = (int64_t)cm.frame_bytes;
+      dev[k].dst_frame_stride = (int64_t)cm.frame_bytes;
     }
-    int rc = adct_compress_quant_planes(dev, n_planes, m, qtab, p->d_sse + f0 * n_planes, s);
-    if (rc != ADCT_OK) return rc;
-    for (int k = 0; k < n_planes; ++k) {
-      const adct_plane_t& q = hp[k];
-      const size_t row = (size_t)q.height * q.width;
-      if (q.dst == nullptr || row == 0) continue;
-      const size_t dfs = m > 1 ? (size_t)q.dst_frame_stride : row;
-      ADCT_CUDA_TRY(cudaMemcpy2DAsync(q.dst + f0 * q.dst_frame_stride, dfs, p->d_out[b] + off[k], frame_bytes,
-                                      row, (size_t)m, cudaMemcpyDeviceToHost, s));
+    if (staged) {
+      segs_out.clear();
+      if (c >= p->depth) {  // slot b still holds chunk c - depth
+        int rc = drain(c - p->depth, false);
+        if (rc != ADCT_OK) return rc;
+      }
+      chunk_segments(cm, f0, m, p->h_in[b], false, segs);
+      segs.insert(segs.end(), segs_out.begin(), segs_out.end());
+      p->pool->run(segs);
+      ADCT_PIPE_TRY(cudaMemcpyAsync(p->d_in[b], p->h_in[b], (size_t)m * cm.frame_bytes, cudaMemcpyHostToDevice, s));
+    } else {
+      for (int k = 0; k < n_planes; ++k) {
+        const adct_plane_t& q = hp[k];
+        const size_t row = (size_t)q.height * q.width;
+        const size_t sfs = m > 1 ? (size_t)q.src_frame_stride : row;
+        if (row)
+          ADCT_PIPE_TRY(cudaMemcpy2DAsync(p->d_in[b] + cm.off[k], cm.frame_bytes, q.src + f0 * q.src_frame_stride,
+                                          sfs, row, (size_t)m, cudaMemcpyHostToDevice, s));
+      }
+    }
+    int rc = launch_chunk(dev, n_planes, m, kind, r, qtab, p->d_sse + f0 * n_planes, s);
+    if (rc != ADCT_OK) return pipeline_fail(p, rc);
+    if (staged) {
+      if (any_dst)
+        ADCT_PIPE_TRY(cudaMemcpyAsync(p->h_out[b], p->d_out[b], (size_t)m * cm.frame_bytes, cudaMemcpyDeviceToHost, s));
+      ADCT_PIPE_TRY(cudaEventRecord(p->done[b], s));
+    } else {
+      for (int k = 0; k < n_planes; ++k) {
+        const adct_plane_t& q = hp[k];
+        const size_t row = (size_t)q.height * q.width;
+        if (q.dst == nullptr || row == 0) continue;
+        const size_t dfs = m > 1 ? (size_t)q.dst_frame_stride : row;
+        ADCT_PIPE_TRY(cudaMemcpy2DAsync(q.dst + f0 * q.dst_frame_stride, dfs, p->d_out[b] + cm.off[k],
+                                        cm.frame_bytes, row, (size_t)m, cudaMemcpyDeviceToHost, s));
+      }
     }
   }
-  for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
-  ADCT_CUDA_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n_frames * n_planes * sizeof(uint64_t),
+  if (staged)
+    for (int64_t c = std::max<int64_t>(0, n_chunks - p->depth); c < n_chunks; ++c) {
+      int rc = drain(c, true);
+      if (rc != ADCT_OK) return rc;
+    }
+  for (int k = 0; k < p->depth; ++k) ADCT_PIPE_TRY(cudaStreamSynchronize(p->stream[k]));
+  ADCT_PIPE_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n_frames * n_planes * sizeof(uint64_t),
                            cudaMemcpyDeviceToHost));
   return ADCT_OK;
 }
 
-// kind: 0 retain (r), 1 quant (qtab)
+// kind: 0 retain (r), 1 quant (qtab) — a batch of single images is one plane.
 int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, int64_t n, int32_t h,
                  int32_t w, int kind, int32_t r, const adct_qtab_t* qtab, uint64_t* host_sse) {
   if (p == nullptr || n < 0) return ADCT_ERR_INVALID_ARGUMENT;
@@ -1026,39 +1184,8 @@ int pipeline_run(adct_pipeline* p, const uint8_t* host_img, uint8_t* host_rec, i
   if (kind == 1 && qtab == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   if (n == 0) return ADCT_OK;
   if (host_img == nullptr || host_sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
-  const int64_t px = (int64_t)h * w;
-  if (px == 0) {
-    std::memset(host_sse, 0, (size_t)n * sizeof(uint64_t));
-    return ADCT_OK;
-  }
-  ADCT_CUDA_TRY(cudaSetDevice(p->device));
-  int rc0 = pipeline_reserve(p, (size_t)px, n);
-  if (rc0 != ADCT_OK) return rc0;
-  const int64_t per = (int64_t)(p->chunk_bytes / (size_t)px);
-  // Chunk i goes to stream i % 3: its H2D, kernel and D2H are ordered on that
-  // stream, and the copy engines overlap chunk i's D2H with chunk i+1's H2D.
-  // Nothing in the loop blocks the host (no pageable-memory copies).
-  int64_t chunk = 0;
-  for (int64_t i0 = 0; i0 < n; i0 += per, ++chunk) {
-    const int b = (int)(chunk % p->depth);
-    const int64_t m = (n - i0) < per ? (n - i0) : per;
-    cudaStream_t s = p->stream[b];
-    ADCT_CUDA_TRY(cudaMemcpyAsync(p->d_in[b], host_img + i0 * px, (size_t)(m * px),
-                                  cudaMemcpyHostToDevice, s));
-    uint8_t* drec = host_rec ? p->d_out[b] : nullptr;
-    int rc;
-    if (kind == 0)
-      rc = adct_compress_retain(p->d_in[b], drec, m, h, w, px, px, r, p->d_sse + i0, nullptr, s);
-    else
-      rc = adct_compress_quant(p->d_in[b], drec, m, h, w, px, px, qtab, p->d_sse + i0, s);
-    if (rc != ADCT_OK) return rc;
-    if (host_rec)
-      ADCT_CUDA_TRY(cudaMemcpyAsync(host_rec + i0 * px, p->d_out[b], (size_t)(m * px),
-                                    cudaMemcpyDeviceToHost, s));
-  }
-  for (int k = 0; k < p->depth; ++k) ADCT_CUDA_TRY(cudaStreamSynchronize(p->stream[k]));
-  ADCT_CUDA_TRY(cudaMemcpy(host_sse, p->d_sse, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  return ADCT_OK;
+  adct_plane_t pl = single_plane(host_img, host_rec, h, w, (int64_t)h * w, (int64_t)h * w);
+  return pipeline_frames_run(p, &pl, 1, n, kind, r, qtab, host_sse);
 }
 
 }  // namespace
@@ -1110,7 +1237,7 @@ int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img, ui
 int adct_pipeline_compress_quant_planes(adct_pipeline_t* p, const adct_plane_t* host_planes,
                                         int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
                                         uint64_t* host_sse) {
-  return pipeline_planes_run(p, host_planes, n_planes, n_frames, qtab, host_sse);
+  return pipeline_frames_run(p, host_planes, n_planes, n_frames, 1, 0, qtab, host_sse);
 }
 
 int adct_quant_jit_stats(int64_t* compiled, int64_t* launches, int64_t* failures) {
@@ -1127,6 +1254,11 @@ int adct_host_register(void* ptr, size_t bytes) {
   if (bytes == 0) return ADCT_OK;
   ADCT_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
   return ADCT_OK;
+}
+
+int adct_host_is_pinned(const void* ptr) {
+  if (ptr == nullptr) return 0;
+  return is_pinned(ptr) ? 1 : 0;
 }
 
 int adct_host_unregister(void* ptr) {

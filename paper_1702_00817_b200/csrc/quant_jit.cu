@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <string>
@@ -59,9 +60,13 @@ struct Driver {
 
 struct Entry {
   int uses = 0;
-  int state = 0;  // 0 generic, 1 specialised, -1 specialisation failed
+  int state = 0;  // 0 generic, 1 specialised, 2 being built (by another thread), -1 specialisation failed
   CUfunction fn = nullptr;
 };
+
+// Tables that are used fewer than the threshold times keep an entry (a use
+// count); past this many entries the never-specialised ones are dropped.
+constexpr size_t kMaxEntries = 256;
 
 std::mutex g_mu;
 std::map<std::string, Entry> g_cache;
@@ -214,25 +219,38 @@ void* quant_function(int kind, const QParamsDev& q, cudaStream_t stream) {
   std::string key(reinterpret_cast<const char*>(&q), sizeof(QParamsDev));
   key.push_back((char)kind);
   key.append(reinterpret_cast<const char*>(&dev), sizeof dev);
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_cache.find(key);
+    if (it == g_cache.end()) {
+      if (g_cache.size() >= kMaxEntries)
+        for (auto jt = g_cache.begin(); jt != g_cache.end();)
+          jt = jt->second.state == 0 ? g_cache.erase(jt) : std::next(jt);
+      it = g_cache.emplace(key, Entry{}).first;
+    }
+    Entry& e = it->second;
+    if (e.state == 1) return e.fn;
+    if (e.state != 0 || capturing) return nullptr;  // failed, or another thread is compiling it
+    if (++e.uses < after) return nullptr;
+    e.state = 2;  // this thread compiles; others keep launching the generic kernel meanwhile
+  }
+  // NVRTC + module load outside the lock: other tables and devices are not
+  // held up for the seconds a compile takes
+  CUfunction fn = build(kind, q);
   std::lock_guard<std::mutex> lock(g_mu);
   Entry& e = g_cache[key];
-  if (e.state == 1) return e.fn;
-  if (e.state < 0 || capturing) return nullptr;
-  if (++e.uses < after) return nullptr;
-  e.fn = build(kind, q);
-  e.state = e.fn ? 1 : -1;
-  (e.fn ? g_compiled : g_failures)++;
-  return e.fn;
+  e.fn = fn;
+  e.state = fn ? 1 : -1;
+  (fn ? g_compiled : g_failures)++;
+  return fn;
 }
 
 int launch(void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, void** args) {
   Driver& dr = driver();
-  if (!dr.ok) return 1;
+  if (!dr.ok) return (int)CUDA_ERROR_NOT_INITIALIZED;
   g_launches++;
-  return dr.launch(reinterpret_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
-                   (unsigned)smem, reinterpret_cast<CUstream>(stream), args, nullptr) == CUDA_SUCCESS
-             ? 0
-             : 1;
+  return (int)dr.launch(reinterpret_cast<CUfunction>(fn), grid.x, grid.y, grid.z, block.x, block.y, block.z,
+                        (unsigned)smem, reinterpret_cast<CUstream>(stream), args, nullptr);
 }
 
 void stats(long long* compiled, long long* launches, long long* failures) {

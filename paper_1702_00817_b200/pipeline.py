@@ -2,8 +2,12 @@
 
 Wraps the native adct_pipeline (csrc/capi.cu): chunks of the host batch are
 copied in, compressed and copied out on three CUDA streams so H2D, kernel
-and D2H overlap.  Host arrays are page-locked for the duration of the call
-(adct_host_register) unless already pinned.
+and D2H overlap.  Ordinary (pageable) numpy arrays are staged by the library
+through its own page-locked ring, filled and drained by host threads while
+the copies run (never registered per call); page-locked arrays
+(`pinned_empty`, or `pin()` for repeated use) are copied directly.
+`register=True` page-locks the caller's arrays for the call instead
+(arrays that are already pinned are left alone).
 """
 
 from __future__ import annotations
@@ -50,11 +54,21 @@ class HostPipeline:
             raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
         return n, h, w
 
-    def compress_retain(self, images: np.ndarray, r: int, rec: np.ndarray | None = None, *, register: bool = True):
+    @staticmethod
+    def _check_rec(rec, images: np.ndarray) -> None:
+        """The native copies write n*h*w bytes at rec: it must be exactly that buffer."""
+        if rec is None:
+            return
+        if not isinstance(rec, np.ndarray) or rec.dtype != np.uint8 or rec.shape != images.shape \
+                or not rec.flags.c_contiguous or not rec.flags.writeable:
+            raise ValueError(f"rec must be a writeable C-contiguous uint8 array of shape {images.shape}")
+
+    def compress_retain(self, images: np.ndarray, r: int, rec: np.ndarray | None = None, *, register: bool = False):
         """Returns (rec or None, sse int64[N])."""
         if not 1 <= int(r) <= 64:
             raise InvalidRetention(f"retention count must be in [1, 64], got {r}")
         n, h, w = self._check(images)
+        self._check_rec(rec, images)
         sse = np.zeros(n, dtype=np.uint64)
         with _Pinned([images, rec] if register else []):
             _lib.call(
@@ -63,8 +77,9 @@ class HostPipeline:
             )
         return rec, sse.astype(np.int64)
 
-    def compress_quant(self, images: np.ndarray, qtab, rec: np.ndarray | None = None, *, register: bool = True):
+    def compress_quant(self, images: np.ndarray, qtab, rec: np.ndarray | None = None, *, register: bool = False):
         n, h, w = self._check(images)
+        self._check_rec(rec, images)
         sse = np.zeros(n, dtype=np.uint64)
         with _Pinned([images, rec] if register else []):
             _lib.call(
@@ -74,7 +89,7 @@ class HostPipeline:
         return rec, sse.astype(np.int64)
 
 
-    def compress_quant_planes(self, planes, qtab, outs=None, *, register: bool = True):
+    def compress_quant_planes(self, planes, qtab, outs=None, *, register: bool = False):
         """Frames of 1..3 host planes (each (N, H_k, W_k) uint8, e.g. Y/Cb/Cr of
         4:2:0 video) through the one-launch planes kernel in chunks of frames.
         `outs`: matching arrays for the reconstructions, or None (SSE only).
@@ -117,9 +132,15 @@ class _Pinned:
         self.done = []
 
     def __enter__(self):
-        for a in self.arrays:
-            _lib.call("adct_host_register", a.ctypes.data, a.nbytes)
-            self.done.append(a)
+        try:
+            for a in self.arrays:
+                if _lib.lib().adct_host_is_pinned(a.ctypes.data):
+                    continue  # already page-locked (pinned_empty / pin()): leave it to its owner
+                _lib.call("adct_host_register", a.ctypes.data, a.nbytes)
+                self.done.append(a)
+        except BaseException:
+            self.__exit__()
+            raise
         return self
 
     def __exit__(self, *exc):

@@ -110,6 +110,11 @@ class SseExchange:
         ex = SseExchange(n_total, device)
         rec, local = ex.compress_retain(images_of_this_rank, r, shard.start)
         ex.sse  # int64 [n_total], identical on every rank after the call
+
+    Each call is bracketed by two stream-ordered symmetric-memory barriers:
+    the one before the pushes keeps a rank from overwriting a peer's vector
+    while the peer's reads of the previous call (enqueued before its own
+    call) are pending; the one after makes every rank's pushes visible.
     """
 
     def __init__(self, n_total: int, device, group=None):
@@ -121,6 +126,7 @@ class SseExchange:
         self.n_total = int(n_total)
         self.sse = symm_mem.empty(self.n_total, dtype=torch.int64, device=device)
         self.sse.zero_()
+        torch.cuda.synchronize(device)  # zeroed before any peer can store into it
         self._hdl = symm_mem.rendezvous(self.sse, group.group_name)
         self.n_peers = int(self._hdl.world_size)
         self._arrivals: torch.Tensor | None = None
@@ -133,6 +139,10 @@ class SseExchange:
             raise ValueError(f"images [{offset}, {offset + n}) outside the exchange vector of {self.n_total}")
         if self._arrivals is None or self._arrivals.numel() < n:
             self._arrivals = torch.zeros(max(n, 1), dtype=torch.int32, device=images.device)
+        # stream-ordered barrier BEFORE the pushes: no rank stores into a peer's
+        # vector while that peer may still read the previous call's values
+        # (its reads were enqueued before its own barrier)
+        self._hdl.barrier(channel=1)
         rec, local = batch.compress_retain_exchange(
             images, r, self._hdl.buffer_ptrs_dev, self.n_peers, offset, self._arrivals, out=out, sse_out=sse_out
         )
@@ -150,6 +160,7 @@ class SseExchange:
             raise ValueError(f"frames [{frame_offset}, {frame_offset + n}) x {k} planes outside the exchange vector")
         if self._arrivals is None or self._arrivals.numel() < n * k:
             self._arrivals = torch.zeros(max(n * k, 1), dtype=torch.int32, device=planes[0].device)
+        self._hdl.barrier(channel=1)  # see compress_retain: no store while a peer may still read
         recs, local = batch.compress_quant_planes_exchange(
             planes, qtab, self._hdl.buffer_ptrs_dev, self.n_peers, off, self._arrivals, out=out
         )

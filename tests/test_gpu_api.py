@@ -180,6 +180,57 @@ def test_host_pipeline_empty_and_degenerate(cuda):
             p.compress_retain(np.zeros((1, 8, 16), np.uint8), 65)
 
 
+@pytest.mark.parametrize("mode", ["pageable", "register", "pinned_in", "pinned_out"])
+def test_host_pipeline_staging_modes(cuda, mode):
+    """Pageable numpy arrays go through the library's page-locked ring (many
+    chunks per call, so every ring slot is reused several times); registered
+    or pinned arrays are copied directly; mixed calls stage.  All exact."""
+    from paper_1702_00817_b200.pipeline import pinned_empty
+
+    imgs = synth.images_np(range(50, 63), 64, 128, 16, 8.0, 64.0)  # 13 images, 8 KiB each
+    src, dst = imgs, np.empty_like(imgs)
+    if mode == "pinned_in":
+        src = pinned_empty(imgs.shape)
+        src[...] = imgs
+    if mode == "pinned_out":
+        dst = pinned_empty(imgs.shape)
+    wr, ws, _ = exact.compress_retain(imgs, 10)
+    qt = quant.quant_table(50)
+    wq, wqs = exact.compress_quant(imgs, quant.qtab_qprime(qt))
+    with HostPipeline(0, chunk_bytes=2 * 8192) as p:  # 2 images per chunk: 7 chunks, 3 slots
+        for rep in range(2):
+            dst[...] = 0
+            _, sse = p.compress_retain(src, 10, dst, register=(mode == "register"))
+            assert np.array_equal(dst, wr) and np.array_equal(sse, ws), (mode, rep)
+            _, sseq = p.compress_quant(src, qt, dst, register=(mode == "register"))
+            assert np.array_equal(dst, wq) and np.array_equal(sseq, wqs), (mode, rep)
+            _, sse_only = p.compress_quant(src, qt)
+            assert np.array_equal(sse_only, wqs)
+
+
+def test_host_pipeline_rejects_bad_rec(cuda):
+    imgs = np.zeros((3, 16, 16), np.uint8)
+    with HostPipeline(0) as p:
+        for bad in (np.zeros((2, 16, 16), np.uint8), np.zeros((3, 16, 16), np.int16),
+                    np.zeros((3, 16, 32), np.uint8)[:, :, ::2]):
+            with pytest.raises(ValueError):
+                p.compress_retain(imgs, 10, bad)
+            with pytest.raises(ValueError):
+                p.compress_quant(imgs, quant.quant_table(50), bad)
+
+
+def test_batch_rejects_bad_out_and_sse(cuda):
+    x = torch.zeros((3, 16, 16), dtype=torch.uint8, device=cuda)
+    with pytest.raises(ValueError):
+        batch.compress_retain(x, 10, out=torch.zeros((2, 16, 16), dtype=torch.uint8, device=cuda))
+    with pytest.raises(ValueError):
+        batch.compress_retain(x, 10, sse_out=torch.zeros(4, dtype=torch.int64, device=cuda))
+    with pytest.raises(ValueError):
+        batch.compress_quant(x, quant.quant_table(50), sse_out=torch.zeros((3, 2), dtype=torch.int64, device=cuda)[:, 0])
+    with pytest.raises(ValueError):
+        batch.compress_quant(x, quant.quant_table(50), out=torch.zeros((3, 16, 16), dtype=torch.int32, device=cuda))
+
+
 def test_pinned_empty_buffers_through_pipeline(cuda):
     import gc
 

@@ -3,7 +3,7 @@
 On one GPU the multi-peer push is exercised with several local vectors as
 the "peers" (no kernel waits on another), and the torch symmetric-memory
 wrapper (`shard.SseExchange`) at world size 1 in a child process.  Results
-must equal adct_compress_retain's exact SSE."""
+must equal the C oracle's exact SSE (oracle/fast.py)."""
 
 import os
 import subprocess
@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 import torch
 
+from oracle import fast
 from paper_1702_00817_b200 import batch, synth
 
 pytestmark = pytest.mark.gpu
@@ -24,11 +25,18 @@ def _peer_array(vectors):
     return ptrs
 
 
-@pytest.mark.parametrize("shape", [(6, 64, 256), (5, 40, 24), (3, 256, 2048)])
-def test_exchange_matches_retain_on_local_peers(cuda, shape):
+@pytest.mark.parametrize("packed", ["1", "0"])
+@pytest.mark.parametrize("shape", [(6, 64, 256), (5, 40, 24), (3, 256, 2048), (2, 1024, 1024)])
+def test_exchange_matches_oracle_on_local_peers(cuda, shape, packed, monkeypatch):
+    """Both epilogue forms — the CTA count packed into the SSE word, and the
+    fenced per-image arrival counter (ADCT_XCHG_PACKED=0, the path for images
+    of >= 2^16 CTAs) — against the C oracle, repeated (counters reset)."""
+    monkeypatch.setenv("ADCT_XCHG_PACKED", packed)
     n, h, w = shape
     x = synth.images_device(range(40, 40 + n), h, w, 16, 8.0, 64.0, device=cuda)
-    rec_ref, sse_ref, _ = batch.compress_retain(x, 10)
+    rec_o, sse_o, _ = fast.compress_retain(x.cpu().numpy(), 10)
+    rec_ref = torch.from_numpy(rec_o).to(cuda)
+    sse_ref = torch.from_numpy(sse_o).to(cuda)
     offset, total = 7, n + 11
     peers = [torch.full((total,), -5, dtype=torch.int64, device=cuda) for _ in range(3)]
     ptrs = _peer_array(peers)
@@ -68,8 +76,9 @@ import torch, torch.distributed as dist
 from paper_1702_00817_b200 import batch, shard, synth
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+from oracle import fast
 x = synth.images_device(range(9), 256, 256, 16, 8.0, 64.0, device="cuda")
-_, want, _ = batch.compress_retain(x, 10)
+want = torch.from_numpy(fast.compress_retain(x.cpu().numpy(), 10, rec=False)[1]).cuda()
 ex = shard.SseExchange(12, "cuda")
 for rep in range(2):
     rec, local = ex.compress_retain(x[:5], 10, 0)
@@ -80,7 +89,8 @@ for rep in range(2):
 from paper_1702_00817_b200 import quant
 planes = [x[:, :128, :].contiguous(), x[:, :64, :128].contiguous(), x[:, 64:128, 128:].contiguous()]
 qt = quant.quant_table(75)
-_, wantq = batch.compress_quant_planes(planes, qt)
+wantq = torch.stack([torch.from_numpy(fast.compress_quant(p.cpu().numpy(), quant.qtab_qprime(qt), rec=False)[1])
+                     for p in planes], dim=1).cuda()
 exq = shard.SseExchange(9 * 3 + 3, "cuda")
 exq.compress_quant_planes([p[:4] for p in planes], qt, 0)
 exq.compress_quant_planes([p[4:] for p in planes], qt, 4)
@@ -106,7 +116,10 @@ def test_quant_planes_exchange_on_local_peers(cuda, q, cr_w):
     cb = torch.randint(0, 256, (4, 24, 48), dtype=torch.uint8, generator=g).to(cuda)
     cr = torch.randint(0, 256, (4, 24, cr_w), dtype=torch.uint8, generator=g).to(cuda)
     qt = quant.quant_table(q)
-    recs_ref, sse_ref = batch.compress_quant_planes([y, cb, cr], qt)
+    qp = quant.qtab_qprime(qt)
+    outs = [fast.compress_quant(p.cpu().numpy(), qp) for p in (y, cb, cr)]
+    recs_ref = [torch.from_numpy(o[0]).to(cuda) for o in outs]
+    sse_ref = torch.from_numpy(np.stack([o[1] for o in outs], axis=1)).to(cuda)
     offset, total = 6, 4 * 3 + 9
     peers = [torch.full((total,), -5, dtype=torch.int64, device=cuda) for _ in range(2)]
     ptrs = _peer_array(peers)

@@ -222,7 +222,9 @@ def test_empty_batch(cuda):
 
 
 @pytest.mark.parametrize("env", [{"ADCT_QUANT_KERNEL": "grid"}, {"ADCT_WIDE_KERNEL": "scalar"},
-                                 {"ADCT_PIPELINE_DEPTH": "2"}])
+                                 {"ADCT_PIPELINE_DEPTH": "2"}, {"ADCT_QUANT_FLOAT": "0"},
+                                 {"ADCT_QUANT_FLOAT": "0", "ADCT_WIDE_KERNEL": "scalar"},
+                                 {"ADCT_PIPELINE_THREADS": "1"}, {"ADCT_QUANT_JIT_AFTER": "1"}])
 def test_alternate_kernel_paths(cuda, env):
     """The A/B switches keep their kernels exact: one-tile-per-CTA quant
     kernel, scalar coarse-table kernel, a 2-deep host pipeline (child process:
@@ -241,7 +243,7 @@ from paper_1702_00817_b200.pipeline import HostPipeline
 g = torch.Generator().manual_seed(3)
 for shape in ((3, 64, 256), (2, 40, 24)):
     x = torch.randint(0, 256, shape, dtype=torch.uint8, generator=g)
-    for q in (10, 30, 75):
+    for q in (2, 10, 30, 75, 95):
         qt = quant.quant_table(q)
         rec, sse = batch.compress_quant(x.cuda(), qt)
         wr, ws = exact.compress_quant(x.numpy(), quant.qtab_qprime(qt))
