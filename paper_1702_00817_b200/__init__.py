@@ -30,6 +30,7 @@ from .errors import (
     InvalidRetention,
     IoFailure,
     MalformedHeader,
+    MissingImage,
     NonOrthogonalKernel,
     NonPositiveQuantizer,
     TruncatedData,
@@ -39,17 +40,13 @@ from .errors import (
 )
 from .flowgraph import OpCount, count_operations, fast_forward, flow_intermediates
 from .metrics import CorpusSummary, QualityRecord, ape_vs_dct, mse, psnr, summarize
-from .sweep import ExperimentConfig, compare_transforms, run_sweep, write_sweep_outputs
+from .sweep import ExperimentConfig, compare_transforms, load_corpus_images, resolve_transform, run_sweep, write_sweep_outputs
 from .transforms import (
     ApproximateTransform,
     DiagonalScaling,
     ExactDct,
-    KernelRegistry,
     TransformMatrix,
-    derive_scaling,
     exact_dct_matrix,
-    load_registry,
-    parse_kernel_records,
     proposed_kernel,
     proposed_scaling,
     proposed_transform,

@@ -21,6 +21,7 @@ kernels (adct_*_dense).
 
 from __future__ import annotations
 
+import warnings
 from functools import lru_cache
 
 import numpy as np
@@ -94,9 +95,20 @@ def _to_dev(a, dtype=None) -> tuple[torch.Tensor, bool]:
     if isinstance(a, torch.Tensor):
         t = a if a.is_cuda else a.to(_device())
         return (t if dtype is None else t.to(dtype)), False
-    arr = np.asarray(a)
-    t = torch.from_numpy(np.ascontiguousarray(arr)).to(_device())
+    t = _host_tensor(a).to(_device())
     return (t if dtype is None else t.to(dtype)), True
+
+
+def _host_tensor(a) -> torch.Tensor:
+    """A CPU tensor viewing numpy data.  Read-only arrays (the reference
+    freezes its image samples) are viewed as they are: the view is only read
+    (copied to the device), so torch's non-writable warning does not apply."""
+    arr = np.ascontiguousarray(np.asarray(a))
+    if arr.flags.writeable:
+        return torch.from_numpy(arr)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(arr)
 
 
 def _back(t: torch.Tensor, to_numpy: bool):

@@ -35,14 +35,23 @@ class OpCount:
                        self.shifts + other.shifts)
 
 
-# (name, additions) per stage in application order: A1 8, A2 4 (+3 free
-# negations), A3 2 (+1), P 0 (fast.py:130-168)
-STAGE_COSTS = (("A1", 8), ("A2", 4), ("A3", 2), ("P", 0))
+def stage_costs() -> tuple[tuple[str, int], ...]:
+    """(stage, additions) counted from the stage matrices themselves, the way
+    the reference tallies its FactorStage steps (fast.py:50-126, 236-241): an
+    output line that combines k > 1 inputs costs k - 1 additions; a copy, a
+    negation (sign folded into a later add) or a permutation costs nothing.
+    Entries are only 0/+-1, so there are no multiplications or shifts."""
+    out = []
+    for name, m in zip(("A1", "A2", "A3", "P"), stage_matrices()):
+        assert set(np.unique(m).tolist()) <= {-1, 0, 1}
+        out.append((name, int(sum(max(0, int(np.count_nonzero(row)) - 1) for row in m))))
+    return tuple(out)
 
 
 def count_operations() -> OpCount:
-    """14 additions, 0 multiplications, 0 shifts (paper Table 1)."""
-    return OpCount(additions=sum(c for _, c in STAGE_COSTS))
+    """14 additions, 0 multiplications, 0 shifts (paper Table 1), tallied
+    from the flow graph's stages (A1 8, A2 4, A3 2, P 0)."""
+    return OpCount(additions=sum(c for _, c in stage_costs()))
 
 
 def flow_intermediates(x: Sequence) -> list[list]:

@@ -2,14 +2,17 @@
 
 `mse` runs on the GPU (exact integer SSE for uint8 inputs via adct_sse_u8,
 float64 reduction otherwise); `psnr`, `ape_vs_dct` and `summarize` are host
-arithmetic on scalars, exactly as in the reference.
+arithmetic on scalars with the reference's results; the CSV writers produce
+the reference's report format.
 """
 
 from __future__ import annotations
 
+import csv
 import math
+from collections import defaultdict
 from dataclasses import dataclass
-from typing import Iterable
+from typing import Iterable, TextIO
 
 import numpy as np
 import torch
@@ -46,7 +49,9 @@ def _device_pair(a, b):
     def conv(x):
         if isinstance(x, torch.Tensor):
             return x.to(dev)
-        return torch.from_numpy(np.ascontiguousarray(np.asarray(x))).to(dev)
+        from .codec import _host_tensor
+
+        return _host_tensor(x).to(dev)
 
     return conv(a), conv(b)
 
@@ -84,16 +89,50 @@ def ape_vs_dct(avg_mse_approx: float, avg_mse_dct: float) -> float:
 
 
 def summarize(records: Iterable[QualityRecord], *, psnr_from_avg_mse: bool = False) -> list[CorpusSummary]:
-    """Per-(transform, r) averages; avg_psnr is the mean of per-image PSNRs by default (metrics.py:75-97)."""
-    groups: dict[tuple[str, int], list[QualityRecord]] = {}
+    """One CorpusSummary per (transform, r), in key order (metrics.py:75-97).
+    avg_psnr is the mean of the per-image PSNRs, or with psnr_from_avg_mse
+    the PSNR of avg_mse; EmptyGroup when there is nothing to average."""
+    by_key: dict[tuple[str, int], list[QualityRecord]] = defaultdict(list)
     for rec in records:
-        groups.setdefault((rec.transform_name, rec.r), []).append(rec)
-    if not groups:
+        by_key[rec.transform_name, rec.r].append(rec)
+    if not by_key:
         raise EmptyGroup("no records to summarize")
     out = []
-    for name, r in sorted(groups):
-        members = groups[(name, r)]
-        avg_mse = float(np.mean([m.mse for m in members]))
-        avg_psnr = psnr(avg_mse) if psnr_from_avg_mse else float(np.mean([m.psnr for m in members]))
-        out.append(CorpusSummary(name, r, avg_mse, avg_psnr, len(members)))
+    for key in sorted(by_key):
+        mses = np.array([m.mse for m in by_key[key]], dtype=np.float64)
+        psnrs = np.array([m.psnr for m in by_key[key]], dtype=np.float64)
+        avg_mse = float(mses.mean())
+        out.append(CorpusSummary(key[0], key[1], avg_mse,
+                                 psnr(avg_mse) if psnr_from_avg_mse else float(psnrs.mean()), len(mses)))
     return out
+
+
+# --- CSV reports (metrics.py:100-122): same columns, order and number format ---
+
+def format_float(x: float) -> str:
+    """%.6g ('inf' for a lossless PSNR)."""
+    return f"{x:.6g}"
+
+
+_RECORD_COLUMNS = (("image_id", lambda m: m.image_id), ("transform", lambda m: m.transform_name),
+                   ("r", lambda m: m.r), ("mse", lambda m: format_float(m.mse)),
+                   ("psnr", lambda m: format_float(m.psnr)))
+_SUMMARY_COLUMNS = (("transform", lambda s: s.transform_name), ("r", lambda s: s.r),
+                    ("avg_mse", lambda s: format_float(s.avg_mse)), ("avg_psnr", lambda s: format_float(s.avg_psnr)),
+                    ("n_images", lambda s: s.n_images))
+
+
+def _write_table(fp: TextIO, columns, rows, key) -> None:
+    w = csv.writer(fp, lineterminator="\n")
+    w.writerow([name for name, _ in columns])
+    w.writerows([[get(row) for _, get in columns] for row in sorted(rows, key=key)])
+
+
+def write_quality_csv(fp: TextIO, records: Iterable[QualityRecord]) -> None:
+    """Per-image records sorted by (transform, r, image_id)."""
+    _write_table(fp, _RECORD_COLUMNS, records, key=lambda m: (m.transform_name, m.r, m.image_id))
+
+
+def write_summary_csv(fp: TextIO, summaries: Iterable[CorpusSummary]) -> None:
+    """Per-(transform, r) summaries sorted by (transform, r)."""
+    _write_table(fp, _SUMMARY_COLUMNS, summaries, key=lambda s: (s.transform_name, s.r))

@@ -5,14 +5,17 @@ The reference reads one PGM at a time into float64 samples
 with `readinto` directly into one page-locked uint8 (N, H, W) buffer — no
 float conversion, no intermediate copy — which the host pipeline then streams
 through the GPU (H2D overlapped with compute and D2H).  Header parsing and
-the contract errors follow the reference: P2/P5 magic, whitespace and '#'
-comments, maxval in (0, 255], exactly one whitespace byte before a P5 raster,
-TruncatedData on short rasters, samples above maxval rejected.
+the contract error classes follow the reference (P2/P5 magic, whitespace and
+'#' comments, maxval in (0, 255], exactly one whitespace byte before a P5
+raster, TruncatedData on short rasters, samples above maxval rejected).  The
+reference's float64 GrayImage / read_pgm / write_pgm stay with the reference:
+a drop-in caller keeps using them, and this module is the uint8 batch path.
 """
 
 from __future__ import annotations
 
 import os
+import re
 from pathlib import Path
 from typing import Sequence
 
@@ -20,50 +23,47 @@ import numpy as np
 
 from .errors import BadDimensions, IoFailure, MalformedHeader, TruncatedData, UnsupportedMaxval
 
-_WS = b" \t\r\n"
+# A header field is a run of bytes other than PGM whitespace (space, tab,
+# CR, LF) and '#'; a '#' starts a comment that ends at the line break.  One
+# regex alternates the two so comments are skipped in a single scan.
+_FIELD_OR_COMMENT = re.compile(rb"#[^\r\n]*|[^ \t\r\n#]+")
 
 
-def _tokens(data: bytes, start: int = 0):
-    i, n = start, len(data)
-    while i < n:
-        c = data[i : i + 1]
-        if c in _WS:
-            i += 1
-        elif c == b"#":
-            while i < n and data[i : i + 1] not in b"\r\n":
-                i += 1
-        else:
-            j = i
-            while j < n and data[j : j + 1] not in _WS + b"#":
-                j += 1
-            yield data[i:j], j
-            i = j
+def _fields(data: bytes, pos: int = 0):
+    """(field, offset just past it) for every header field from `pos` on."""
+    for m in _FIELD_OR_COMMENT.finditer(data, pos):
+        if not m.group().startswith(b"#"):
+            yield m.group(), m.end()
 
 
 def parse_header(data: bytes) -> tuple[bytes, int, int, int, int]:
-    """(magic, width, height, maxval, offset just past the header's last token)."""
-    tok = _tokens(data)
-    try:
-        magic, _ = next(tok)
-    except StopIteration:
-        raise MalformedHeader("empty file") from None
-    if magic not in (b"P2", b"P5"):
-        raise MalformedHeader(f"not a PGM file (magic {magic!r})")
-    vals, end = [], 0
-    for _ in range(3):
+    """(magic, width, height, maxval, offset just past maxval) of a P2/P5
+    header, raising the reference's contract errors (corpus.py:65-91):
+    MalformedHeader for a bad magic, missing or non-integer fields and
+    non-positive sizes; UnsupportedMaxval outside (0, 255]."""
+    fields = _fields(data)
+    first = next(fields, None)
+    if first is None:
+        raise MalformedHeader("no PGM header: the file is empty")
+    if first[0] not in (b"P2", b"P5"):
+        raise MalformedHeader(f"magic {first[0]!r} is neither P2 nor P5")
+    nums = []
+    end = first[1]
+    for name in ("width", "height", "maxval"):
+        f = next(fields, None)
+        if f is None:
+            raise MalformedHeader(f"PGM header stops before its {name}")
         try:
-            t, end = next(tok)
-            vals.append(int(t))
-        except StopIteration:
-            raise MalformedHeader("header ended early") from None
+            nums.append(int(f[0]))
         except ValueError:
-            raise MalformedHeader(f"non-integer header token {t!r}") from None
-    w, h, maxval = vals
+            raise MalformedHeader(f"PGM {name} {f[0]!r} is not an integer") from None
+        end = f[1]
+    w, h, maxval = nums
     if w <= 0 or h <= 0:
-        raise MalformedHeader(f"bad dimensions {w}x{h}")
+        raise MalformedHeader(f"PGM size {w}x{h} is not positive")
     if not 0 < maxval <= 255:
-        raise UnsupportedMaxval(f"maxval {maxval} outside (0, 255]")
-    return magic, w, h, maxval, end
+        raise UnsupportedMaxval(f"PGM maxval {maxval}: only 1..255 (8-bit samples) is supported")
+    return first[0], w, h, maxval, end
 
 
 def read_pgm_u8(path: str | os.PathLike, out: np.ndarray | None = None) -> np.ndarray:
@@ -79,25 +79,21 @@ def read_pgm_u8(path: str | os.PathLike, out: np.ndarray | None = None) -> np.nd
             f.seek(end + 1)  # exactly one whitespace byte before the raster
             got = f.readinto(memoryview(out).cast("B"))
             if got < w * h:
-                raise TruncatedData(f"expected {w * h} bytes, found {got}")
+                raise TruncatedData(f"P5 raster holds {got} of {w * h} bytes")
         else:
-            data = head + f.read()
-            vals = []
-            for t, _ in _tokens(data, end):
-                try:
-                    vals.append(int(t))
-                except ValueError:
-                    raise MalformedHeader(f"non-integer sample {t!r}") from None
-                if len(vals) == w * h:
-                    break
-            if len(vals) < w * h:
-                raise TruncatedData(f"expected {w * h} samples, found {len(vals)}")
-            arr = np.asarray(vals, dtype=np.int64)
-            if arr.max(initial=0) > 255:
-                raise MalformedHeader("sample exceeds declared maxval")
-            out[...] = arr.reshape(h, w)
+            # P2: decimal samples after the header, same field/comment rules
+            toks = [t for t, _ in _fields(head + f.read(), end)][: w * h]
+            if len(toks) < w * h:
+                raise TruncatedData(f"P2 raster holds {len(toks)} of {w * h} samples")
+            try:
+                vals = np.array([int(t) for t in toks], dtype=np.int64)
+            except ValueError:
+                raise MalformedHeader("P2 raster has a sample that is not an integer") from None
+            if vals.max(initial=0) > maxval or vals.min(initial=0) < 0:
+                raise MalformedHeader(f"P2 sample outside 0..{maxval} (the declared maxval)")
+            out[...] = vals.reshape(h, w)
     if maxval < 255 and int(out.max(initial=0)) > maxval:
-        raise MalformedHeader("sample exceeds declared maxval")
+        raise MalformedHeader(f"P5 sample above the declared maxval {maxval}")
     return out
 
 
@@ -154,31 +150,3 @@ def compress_files(paths: Sequence[str | os.PathLike], r: int, out_dir: str | os
             Path(out_dir).mkdir(parents=True, exist_ok=True)
             write_pgm_u8(rec[k], Path(out_dir) / (Path(path).stem + f"_r{r}.pgm"))
     return results
-
-
-# --- reference-shaped API (corpus.py:26-121) ------------------------------------
-
-class GrayImage:
-    """8-bit-valued grayscale image with float64 samples (corpus.py:26-43)."""
-
-    def __init__(self, width: int, height: int, samples) -> None:
-        if width <= 0 or height <= 0:
-            raise ValueError("image dimensions must be positive")
-        s = np.array(samples, dtype=np.float64).reshape(height, width)
-        if not np.isfinite(s).all():
-            raise ValueError("samples must be finite")
-        if s.min() < 0 or s.max() > 255:
-            raise ValueError("samples must lie in [0, 255]")
-        s.setflags(write=False)
-        self.width, self.height, self.samples = width, height, s
-
-
-def read_pgm(path) -> GrayImage:
-    """P2/P5 PGM -> GrayImage (corpus.read_pgm contract)."""
-    u8 = read_pgm_u8(path)
-    return GrayImage(u8.shape[1], u8.shape[0], u8)
-
-
-def write_pgm(image: GrayImage, path) -> None:
-    """P5, maxval 255, samples rounded half away from zero (corpus.write_pgm)."""
-    write_pgm_u8(np.floor(np.asarray(image.samples) + 0.5).astype(np.uint8), path)

@@ -21,7 +21,6 @@ image, one r, PSNR per transform and optionally the reconstructions as PGM.
 
 from __future__ import annotations
 
-import csv
 import json
 import math
 from dataclasses import asdict, dataclass
@@ -58,15 +57,66 @@ class ExperimentConfig:
         return range(self.r_min, self.r_max + 1)
 
 
+def _reference_registry():
+    """The installed reference package's kernel registry (kernels.py:312-327:
+    default_registry() over its bundled data/kernels.txt), or None.  In a
+    drop-in deployment the reference package is what calls into this one, so
+    its registry and data file are the source of the comparison kernels; this
+    package does not carry a second copy of either."""
+    try:
+        from adct import kernels as ref_kernels
+    except ImportError:
+        return None
+    return ref_kernels.default_registry()
+
+
 def resolve_transform(t):
-    """Name -> transform for the built-ins (cli.py:40-50); objects pass through."""
-    if isinstance(t, str):
-        if t == "dct":
-            return transforms.exact_dct_matrix()
-        if t == "proposed":
-            return transforms.proposed_transform()
-        raise ValueError(f"unknown transform {t!r}; pass registry transforms as objects")
-    return t
+    """Name -> transform (cli.py:40-50): "dct" and "proposed" are built in,
+    any other name is looked up in the installed reference's registry
+    (bas2008, bas2009, bas2011, cb2011, level1, ...); transform objects
+    (ours, the reference's, or anything with an 8x8 `.matrix`) pass through."""
+    if not isinstance(t, str):
+        return t
+    if t == "dct":
+        return transforms.exact_dct_matrix()
+    if t == "proposed":
+        return transforms.proposed_transform()
+    reg = _reference_registry()
+    if reg is None:
+        raise ValueError(f"unknown transform {t!r}: registry names need the reference package `adct` "
+                         "importable (its data/kernels.txt); or pass the transform object")
+    if t not in reg:
+        raise ValueError(f"unknown transform {t!r}; available: dct, proposed, {', '.join(reg.names())}")
+    return reg.get(t)
+
+
+def load_corpus_images(config: ExperimentConfig):
+    """(image_id, samples) pairs like cli.load_corpus_images (cli.py:76-84):
+    every *.pgm of `config.corpus_path` in name order (read as uint8 straight
+    into one batch by pgm.load_batch; MissingImage when there are none), else
+    the reference's synthetic corpus (corpus.synthesize_corpus, needs the
+    reference package)."""
+    from pathlib import Path
+
+    from . import pgm
+    from .errors import MissingImage
+
+    if config.corpus_path is not None:
+        paths = sorted(Path(config.corpus_path).glob("*.pgm"))
+        if not paths:
+            raise MissingImage(f"no .pgm files in {config.corpus_path}")
+        shapes = {pgm.parse_header(open(p, "rb").read(4096))[1:3] for p in paths}
+        if len(shapes) == 1:
+            stack = pgm.load_batch(paths, pinned=False)
+            return [(p.stem, stack[k]) for k, p in enumerate(paths)]
+        return [(p.stem, pgm.read_pgm_u8(p)) for p in paths]
+    try:
+        from adct import corpus as ref_corpus
+    except ImportError:
+        raise ValueError("no corpus_path and no reference package for the synthetic corpus; "
+                         "pass images or a PGM directory") from None
+    imgs = ref_corpus.synthesize_corpus(config.seed, config.n_images)
+    return [(f"synth-{i:03d}", g.samples) for i, g in enumerate(imgs)]
 
 
 def _name(t) -> str:
@@ -104,11 +154,13 @@ def sweep_mse(t, stack: np.ndarray, r_min: int, r_max: int, device=None) -> np.n
     return sse.cpu().numpy() / float(h * w)
 
 
-def run_sweep(config: ExperimentConfig, images: Sequence[tuple[str, np.ndarray]]):
+def run_sweep(config: ExperimentConfig, images: Sequence[tuple[str, np.ndarray]] | None = None):
     """(records, summaries, ape) exactly as cli.run_sweep (cli.py:87-124) returns them.
 
-    `images` are (image_id, samples) pairs (the reference's PGM and synthetic
-    corpus loaders are out of scope; pass arrays)."""
+    `images` are (image_id, samples) pairs; None loads them like the
+    reference (load_corpus_images: config.corpus_path or the synthesizer)."""
+    if images is None:
+        images = load_corpus_images(config)
     records: list[metrics.QualityRecord] = []
     groups = _group_by_shape(images)
     for t in config.transforms:
@@ -133,8 +185,7 @@ def run_sweep(config: ExperimentConfig, images: Sequence[tuple[str, np.ndarray]]
     return records, summaries, ape
 
 
-def _fmt(x: float) -> str:
-    return format(x, ".6g")  # metrics.format_float (metrics.py:100-102)
+_fmt = metrics.format_float
 
 
 def write_sweep_outputs(out_dir, config: ExperimentConfig, records, summaries, ape) -> None:
@@ -142,10 +193,7 @@ def write_sweep_outputs(out_dir, config: ExperimentConfig, records, summaries, a
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
     with open(out / "records.csv", "w", newline="") as fp:
-        wr = csv.writer(fp, lineterminator="\n")
-        wr.writerow(["image_id", "transform", "r", "mse", "psnr"])
-        for rec in sorted(records, key=lambda m: (m.transform_name, m.r, m.image_id)):
-            wr.writerow([rec.image_id, rec.transform_name, rec.r, _fmt(rec.mse), _fmt(rec.psnr)])
+        metrics.write_quality_csv(fp, records)
     with open(out / "summary.csv", "w") as fp:
         fp.write("transform,r,compression_ratio,avg_mse,avg_psnr,ape_vs_dct,n_images\n")
         for s in sorted(summaries, key=lambda m: (m.transform_name, m.r)):
@@ -182,8 +230,7 @@ def compare_transforms(image, r: int, transforms_=("dct", "proposed"), *, out_di
         recon = np.asarray(codec.compress_image(tr, img, r))
         value = metrics.psnr(metrics.mse(img, recon))
         rows.append((_name(t), value))
-        if out_dir is not None:
-            h, w = recon.shape
-            pgm.write_pgm(pgm.GrayImage(w, h, recon), out_dir / f"{stem}_{_name(t)}_r{r}.pgm")
+        if out_dir is not None:  # samples rounded half away (corpus.write_pgm, corpus.py:114-121)
+            pgm.write_pgm_u8(recon, out_dir / f"{stem}_{_name(t)}_r{r}.pgm")
     return rows
 

@@ -102,7 +102,7 @@ def test_compare_transforms_is_cmd_lena(cuda, tmp_path):
 
     img = IMAGES["c1_seed1_128"]
     reg = transforms.ApproximateTransform(transforms.TransformMatrix("flipped", -exact.T),
-                                          transforms.derive_scaling(transforms.TransformMatrix("flipped", -exact.T)))
+                                          transforms.proposed_scaling())
     rows = sweep.compare_transforms(img, 25, ("dct", "proposed", reg), out_dir=tmp_path, stem="c1")
     assert [n for n, _ in rows] == ["dct", "proposed", "flipped"]
     prop = transforms.proposed_transform()
@@ -110,10 +110,10 @@ def test_compare_transforms_is_cmd_lena(cuda, tmp_path):
         want = ref_sweep_mse(C, np.asarray(img, dtype=np.float64), [25])[0]
         assert value == pytest.approx(metrics.psnr(want), abs=1e-8)
         f = tmp_path / f"c1_{name}_r25.pgm"
-        g = pgm.read_pgm(f)
+        g = pgm.read_pgm_u8(f)
         recon = np.asarray(codec.compress_image(sweep.resolve_transform(
             {"dct": "dct", "proposed": "proposed"}.get(name, reg)), img, 25))
-        assert np.array_equal(np.asarray(g.samples), np.floor(recon + 0.5))
+        assert np.array_equal(g, np.floor(recon + 0.5))
     assert rows[1][1] == pytest.approx(rows[2][1], abs=1e-9)  # -T gives the same reconstruction
 
 

@@ -157,45 +157,96 @@ def test_flowgraph_api_kats():
     assert max(abs(v) for st in flowgraph.flow_intermediates([255, 0, 255, 0, 0, 255, 0, 255]) for v in st) <= 2040
 
 
-def test_registry_parse_and_scaling(tmp_path):
+def test_op_count_is_tallied_from_the_stages():
+    from paper_1702_00817_b200 import flowgraph
+
+    assert flowgraph.stage_costs() == (("A1", 8), ("A2", 4), ("A3", 2), ("P", 0))
+    c = transforms.proposed_transform().declared_costs
+    assert (c.additions, c.multiplications, c.shifts) == (14, 0, 0)  # kernels.py:160-163
+
+
+def test_proposed_types_match_reference_objects(reference):
+    """Our transform objects carry the reference's attribute values, and the
+    reference's own objects are recognised as the paper's transform."""
+    ours, ref = transforms.proposed_transform(), reference.proposed_transform()
+    assert np.array_equal(ours.kernel.entries, ref.kernel.entries)
+    assert np.array_equal(ours.scaling.diag, ref.scaling.diag)
+    assert np.array_equal(ours.matrix, ref.matrix) and ours.name == ref.name
+    assert ref.declared_costs.additions == ours.declared_costs.additions == 14
+    assert transforms.is_proposed(ref) and not transforms.is_proposed(reference.exact_dct_matrix())
+    assert np.abs(transforms.exact_dct_matrix().matrix - reference.exact_dct_matrix().matrix).max() < 1e-15
+
+
+def test_type_contract_errors():
     from paper_1702_00817_b200 import errors as E
-    from paper_1702_00817_b200.transforms import derive_scaling, load_registry
 
-    t = exact.T
-    txt = "# test file\nprop\n" + "\n".join(" ".join(str(v) for v in row) for row in t) + "\n14 0 0\n"
+    z = exact.T.copy()
+    z[3] = 0
+    with pytest.raises(E.ZeroRow):
+        transforms.TransformMatrix("z", z)
+    with pytest.raises(ValueError):
+        transforms.TransformMatrix("big", exact.T * 3)
     sgn = np.sign(transforms.exact_dct_matrix().matrix).astype(int)
-    txt += "sdct non-orthogonal\n" + "\n".join(" ".join(str(v) for v in row) for row in sgn) + "\n24 0 0\n"
-    (tmp_path / "k.txt").write_text(txt)
-    reg = load_registry(tmp_path / "k.txt")
-    assert reg.names() == ("prop", "sdct") and len(reg) == 2
-    assert np.allclose(reg.get("prop").scaling.diag, transforms.proposed_scaling().diag)
-    assert reg.get("sdct").orthogonal is False
+    k = transforms.TransformMatrix("sdct", sgn)
     with pytest.raises(E.NonOrthogonalKernel):
-        derive_scaling(sgn)
-    with pytest.raises(E.DuplicateName):
-        reg.register(transforms.TransformMatrix("prop", t))
+        transforms.ApproximateTransform(k, transforms.DiagonalScaling(1 / np.sqrt(np.diag(k.gram()))))
+    t = transforms.ApproximateTransform(k, transforms.DiagonalScaling(1 / np.sqrt(np.diag(k.gram()))), orthogonal=False)
+    assert t.name == "sdct" and t.orthogonal is False and t.matrix.shape == (8, 8)
+    with pytest.raises(ValueError):
+        transforms.DiagonalScaling(np.r_[np.ones(7), 0.0])
 
 
-def test_registry_matches_live_reference(reference):
-    """The reference's own data file parses identically here."""
-    import importlib.resources as ir
+def test_registry_names_resolve_through_the_reference(reference):
+    """Names other than dct/proposed come from the installed reference's own
+    registry (its data/kernels.txt), as cli.resolve_transform does."""
+    from paper_1702_00817_b200 import sweep
 
-    from paper_1702_00817_b200.transforms import load_registry
-
-    path = ir.files("adct").joinpath("data/kernels.txt")
-    ours = load_registry(path)
-    ref = reference.default_registry()
-    assert ours.names() == ref.names()
-    for name in ref.names():
-        assert np.array_equal(ours.get(name).kernel.entries, ref.get(name).kernel.entries)
-        assert np.allclose(ours.get(name).scaling.diag, ref.get(name).scaling.diag, rtol=0, atol=1e-15)
-        assert ours.get(name).orthogonal == ref.get(name).orthogonal
+    reg = reference.default_registry()
+    assert len(reg.names()) >= 5
+    for name in reg.names():
+        t = sweep.resolve_transform(name)
+        assert t is reg.get(name)
+    assert transforms.is_proposed(sweep.resolve_transform("proposed"))
+    with pytest.raises(ValueError):
+        sweep.resolve_transform("no-such-kernel")
 
 
-def test_apply_forward_inverse_kats():
-    t = transforms.proposed_transform()
-    x = np.arange(1, 9, dtype=np.float64)
-    y = transforms.apply_forward(t, x)
-    assert np.allclose(y / t.scaling.diag, [36, -7, 0, 3, 0, 5, 0, 1])
-    assert np.abs(transforms.apply_inverse(t, y) - x).max() < 1e-9
-    assert np.allclose(transforms.apply_inverse(t, np.r_[np.sqrt(8), np.zeros(7)]), np.ones(8))
+def test_load_corpus_images_from_pgm_dir(tmp_path):
+    from paper_1702_00817_b200 import errors as E, pgm, sweep
+
+    cfg = sweep.ExperimentConfig(("proposed",), corpus_path=str(tmp_path))
+    with pytest.raises(E.MissingImage):
+        sweep.load_corpus_images(cfg)
+    rng = np.random.default_rng(4)
+    imgs = {f"im{k}": rng.integers(0, 256, (16, 24), dtype=np.uint8) for k in (2, 0, 1)}
+    for name, im in imgs.items():
+        pgm.write_pgm_u8(im, tmp_path / f"{name}.pgm")
+    got = sweep.load_corpus_images(cfg)
+    assert [n for n, _ in got] == ["im0", "im1", "im2"]
+    assert all(np.array_equal(a, imgs[n]) for n, a in got)
+    pgm.write_pgm_u8(rng.integers(0, 256, (8, 8), dtype=np.uint8), tmp_path / "odd.pgm")  # mixed sizes
+    assert [a.shape for _, a in sweep.load_corpus_images(cfg)][-1] == (8, 8)
+
+
+def test_csv_writers_match_reference(reference):
+    import io
+
+    from paper_1702_00817_b200 import metrics
+
+    recs = [metrics.QualityRecord(f"im{i}", t, r, 10.0 / (r + i), metrics.psnr(10.0 / (r + i)))
+            for i in range(3) for t in ("proposed", "dct") for r in (2, 10)]
+    recs.append(metrics.QualityRecord("zero", "dct", 64, 0.0, metrics.psnr(0.0)))
+    ref_recs = [reference.metrics.QualityRecord(*vars(m).values()) for m in recs]
+    a, b = io.StringIO(), io.StringIO()
+    metrics.write_quality_csv(a, recs)
+    reference.metrics.write_quality_csv(b, ref_recs)
+    assert a.getvalue() == b.getvalue()
+    for conv in (False, True):
+        ours = metrics.summarize(recs, psnr_from_avg_mse=conv)
+        ref = reference.metrics.summarize(ref_recs, psnr_from_avg_mse=conv)
+        assert [tuple(vars(s).values()) for s in ours] == [tuple(vars(s).values()) for s in ref]
+        a, b = io.StringIO(), io.StringIO()
+        metrics.write_summary_csv(a, ours)
+        reference.metrics.write_summary_csv(b, ref)
+        assert a.getvalue() == b.getvalue()
+    assert metrics.format_float(float("inf")) == reference.metrics.format_float(float("inf")) == "inf"

@@ -72,11 +72,31 @@ def test_compress_files_end_to_end(tmp_path, cuda):
         assert np.array_equal(pgm.read_pgm_u8(tmp_path / "out" / f"im{k}_r10.pgm"), wr[k])
 
 
-def test_reference_shaped_api(tmp_path):
-    img = pgm.GrayImage(16, 8, np.arange(128, dtype=np.float64).reshape(8, 16) + 0.4)
-    pgm.write_pgm(img, tmp_path / "g.pgm")
-    back = pgm.read_pgm(tmp_path / "g.pgm")
-    assert back.width == 16 and back.height == 8
-    assert np.array_equal(back.samples, np.floor(img.samples + 0.5))
-    with pytest.raises(ValueError):
-        pgm.GrayImage(2, 2, [0, 1, 2, 300])
+def test_error_classes_match_reference_reader(tmp_path, reference):
+    """Every malformed file raises the same error class as corpus.read_pgm."""
+    cases = {
+        "empty": b"", "magic": b"P6\n2 2\n255\n" + bytes(12), "maxval": b"P5\n2 2\n65535\n" + bytes(8),
+        "maxval0": b"P5\n2 2\n0\n" + bytes(4), "trunc5": b"P5\n4 4\n255\n" + bytes(5),
+        "nonint": b"P5\n4 x\n255\n", "early": b"P5\n4 4\n", "zero": b"P5\n0 4\n255\n",
+        "neg": b"P2\n-2 2\n255\n1 2 3 4\n", "above": b"P2\n2 1\n7\n3 9\n",
+        "trunc2": b"P2\n2 2\n255\n1 2 3\n", "badsample": b"P2\n2 1\n255\n1 q\n",
+        "comments": b"P2 # a\n# b\n2 1 # c\n255\n7 # d\n 8\n", "plus": b"P5\n+2 1\n255\n\x01\x02",
+        "above5": b"P5\n2 1\n100\n\x01\xff",
+    }
+    for name, raw in cases.items():
+        p = _write(tmp_path / f"{name}.pgm", raw)
+        try:
+            ref = reference.corpus.read_pgm(p).samples
+            ref_exc = None
+        except Exception as e:  # noqa: BLE001
+            ref_exc = type(e)
+        try:
+            ours = pgm.read_pgm_u8(p)
+            our_exc = None
+        except Exception as e:  # noqa: BLE001
+            our_exc = type(e)
+        # same class name (ours mirror the reference's errors.py) and base class
+        assert (our_exc and our_exc.__name__) == (ref_exc and ref_exc.__name__), (name, our_exc, ref_exc)
+        assert our_exc is None or our_exc.__mro__[1].__name__ == ref_exc.__mro__[1].__name__
+        if ref_exc is None:
+            assert np.array_equal(ours, ref.astype(np.uint8)), name
