@@ -72,42 +72,56 @@ __device__ __forceinline__ u32 quant_pair(u32 z, int p, const QParamsDev& q) {
 // `zb` is the linear form biased by 0x80008000, i.e. two unsigned 16-bit
 // fields Z + 32768 (|Z| <= 8192, no borrow).  PRMT places each field under
 // the exponent of 2^23, so the two floats are 2^23 + 32768 + Z exactly; one
-// FADD2 removes the offset (exact), one FFMA2 computes RN(M + Z r) with
-// M = 1.5 * 2^23 and r the float just above 1/Q' chosen by adct_qtab_build:
-// r - 1/Q' < 1/(2 Q' 8192) pushes exact ties away from zero and never moves a
-// non-tie across a rounding boundary, so the result is M + round_half_away(Z/Q')
-// (verified exhaustively over |Z| <= 8192 per position by the host).  The
-// result bits are 0x4B400000 + q; packing lanes with a shift and dequantising
-// with one IMAD leaves 0x4B400000 * qe in the product, which the host folds
-// into `wadd`.  Replaces SHF/LOP3 sign logic, the lane split and two
-// IMAD.HI per position (quant_pair below).
-constexpr float kQfMagic = 12582912.0f;                   // 1.5 * 2^23: ulp 1 over [2^23, 2^24)
+// FADD2 removes the offset (exact), one FFMA2 computes RN(M + Z r) with r the
+// float just above 1/Q' chosen by adct_qtab_build: r - 1/Q' < 1/(2 Q' 8192)
+// pushes exact ties away from zero and never moves a non-tie across a
+// rounding boundary, so the result is M + round_half_away(Z/Q') (verified
+// exhaustively over |Z| <= 8192 per position by the host).  M is an even
+// integer in [2^23 + 8192, 2^24 - 8192], where the float grid is the
+// integers, so the result's bits are bits(M) + q.
+// Lane magics: M_A = 1.5 * 2^23 (bits 0x4B400000) and M_B = M_A + 0xB4C0
+// (bits 0x4B40B4C0).  Packing the lanes as qa + (qb << 16) then gives
+//   0x4B400000 + qA + ((0xB4C0 + qB) << 16) = 2^32 + qA + (qB << 16),
+// i.e. exactly the linear form of (qA, qB) mod 2^32: the dequantising IMAD
+// needs no additive constant (no per-position constant register).  This
+// replaces the SHF/LOP3 sign logic, the lane split and two IMAD.HI per
+// position of the integer quantiser (quant_pair below).
+constexpr u32 kQfMagicA = 0x4B400000u;   // 12582912.0f
+constexpr u32 kQfMagicB = 0x4B40B4C0u;   // 12629184.0f
 constexpr unsigned long long kQfOffset = 0x4B0080004B008000ull;  // (2^23 + 32768) in both halves
 constexpr u32 kQfBias = 0x80008000u;                      // +32768 in both 16-bit fields
 
-// The magic M as a run-time value (`small` is a kernel parameter < 256, so the
-// add is 0): ptxas cannot fold it, keeps it in one register and gives FFMA2's
-// immediate slot to r (otherwise every position's r costs a MOV).
-__device__ __forceinline__ float qf_magic(int32_t small) { return __uint_as_float(0x4B400000u + ((u32)small >> 8)); }
+// The lane magics as run-time values (`small` is a kernel parameter < 256, so
+// the adds are 0): ptxas cannot fold them, keeps the pair in two registers
+// and gives FFMA2's immediate slot to r (else every position's r costs a MOV).
+// SAME_LANES: both lanes use M_A (the hybrid kernel dequantises each lane on
+// its own, with the 0x4B400000 * qe offset folded into its scalar wadd).
+template <bool SAME_LANES = false>
+__device__ __forceinline__ unsigned long long qf_magic(int32_t small) {
+  const u32 a = kQfMagicA + ((u32)small >> 8);
+  const u32 b = (SAME_LANES ? kQfMagicA : kQfMagicB) + ((u32)small >> 8);
+  unsigned long long m;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "r"(a), "r"(b));
+  return m;
+}
 
-__device__ __forceinline__ void quant_lanes_f(u32 zb, float r, u32& qa, u32& qb, float magic) {
+__device__ __forceinline__ void quant_lanes_f(u32 zb, float r, u32& qa, u32& qb, unsigned long long magic) {
   const u32 fa = __byte_perm(zb, 0x4B000000u, 0x7610);  // 2^23 + field A
   const u32 fb = __byte_perm(zb, 0x4B000000u, 0x7632);  // 2^23 + field B
-  unsigned long long F, Zf, Q, R, Mm;
+  unsigned long long F, Zf, Q, R;
   asm("mov.b64 %0, {%1, %2};" : "=l"(F) : "r"(fa), "r"(fb));
   asm("mov.b64 %0, {%1, %1};" : "=l"(R) : "f"(r));
-  asm("mov.b64 %0, {%1, %1};" : "=l"(Mm) : "f"(magic));
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(Zf) : "l"(F), "l"(kQfOffset));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(Q) : "l"(Zf), "l"(R), "l"(Mm));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(Q) : "l"(Zf), "l"(R), "l"(magic));
   asm("mov.b64 {%0, %1}, %2;" : "=r"(qa), "=r"(qb) : "l"(Q));
 }
 
 template <class TAB = ParamTab>
-__device__ __forceinline__ u32 quant_pair_f(u32 zb, int p, const QParamsDev& q, float magic) {
+__device__ __forceinline__ u32 quant_pair_f(u32 zb, int p, const QParamsDev& q, unsigned long long magic) {
   const uint4 c = TAB::pos(q, p);  // x: r (float bits), w: qe
   u32 qa, qb;
   quant_lanes_f(zb, __uint_as_float(c.x), qa, qb, magic);
-  return (qa + (qb << 16)) * c.w + TAB::wadd(q, p);
+  return (qa + (qb << 16)) * c.w + TAB::wadd(q, p);  // wadd: 0 except the DC rounding/offset term
 }
 
 // ---------------------------------------------------------------------------
@@ -304,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, ADCT_QP_MINB)
     k_quant_p(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse,
               int64_t n_tiles, u32 tiles_per_frame) {
   extern __shared__ uint4 s_ring[];  // [2][8][kThreads]
-  const float magic = qf_magic(ps.n_planes);
+  const unsigned long long magic = qf_magic(ps.n_planes);
   const int64_t stride = gridDim.x;
   int64_t tile = blockIdx.x;
   if (tile >= n_tiles) return;
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ uint4 s_dyn[];
   uint4* s_orig = s_dyn;                                          // [8][kThreads]
   int* s_wb = reinterpret_cast<int*>(s_dyn + 8 * kThreads);       // [64][kThreads]
-  const float magic = qf_magic(ps.n_planes);
+  const unsigned long long magic = qf_magic<true>(ps.n_planes);
   UnitLoc L;
   u32 acc = 0;
   if (locate_unit<true>(ps, L)) {

@@ -190,9 +190,11 @@ bool to_qparams_hybrid(const adct_qtab_t& t, QParamsDev* q) {
   return true;
 }
 
-// Float-quantiser constants (QF kernels): pos.x = r (float bits), pos.w = qe;
-// the packed result carries 0x4B400000 + q per lane, whose 0x4B400000 * qe
-// is cancelled in wadd.  `scalar`: hybrid kernel offsets (no lane replication).
+// Float-quantiser constants (QF kernels): pos.x = r (float bits), pos.w = qe.
+// Packed kernels: the lane magics make the packed result exactly the linear
+// form (adct_kernels.cuh), so wadd is only the DC rounding/output offset.
+// `scalar` (hybrid kernel, each lane dequantised alone): a lane carries
+// 0x4B400000 + q, whose 0x4B400000 * qe is cancelled in wadd.
 QParamsDev to_qparams_f(const adct_qtab_t& t, bool scalar) {
   QParamsDev q;
   std::memset(&q, 0, sizeof q);
@@ -200,7 +202,7 @@ QParamsDev to_qparams_f(const adct_qtab_t& t, bool scalar) {
   for (int p = 0; p < 64; ++p) {
     q.pos[p].x = t.recip_f[p];
     q.pos[p].w = (uint32_t)t.qe[p];
-    q.wadd[p] = (uint32_t)0 - 0x4B400000u * (uint32_t)t.qe[p];
+    q.wadd[p] = scalar ? (uint32_t)0 - 0x4B400000u * (uint32_t)t.qe[p] : 0u;
   }
   q.wadd[0] += scalar ? 32u + 8192u : (dc_out + 32u) * 65537u;
   return q;

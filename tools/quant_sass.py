@@ -9,7 +9,7 @@ M = 0xFFFFFFFF
 qe = [t.qe[p] for p in range(64)]
 if qf:
     pos = [(t.recip_f[p], 0, 0, qe[p] & M) for p in range(64)]
-    wadd = [(-0x4B400000 * qe[p]) & M for p in range(64)]
+    wadd = [((-0x4B400000 * qe[p]) & M) if kern != "p" else 0 for p in range(64)]
     wadd[0] = (wadd[0] + (((24576 if t.aligned else 32768) + 32) * 65537 if kern == "p" else 32 + 8192)) & M
 else:
     pos = [(t.magic[p], t.mult[p], (t.bias[p] * t.mult[p] * 65537) & M, qe[p] & M) for p in range(64)]
