@@ -493,6 +493,175 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// K3f k_quant_fi: the float-pair inverse.  Any table (q = 10's reconstruction
+// needs 17 bits, beyond the packed kernels' 16-bit lanes).  The forward and
+// the float quantiser run packed as in k_quant_p; from the quantised integers
+// on, the two blocks travel as fp32 pairs (A, B) in 64-bit register pairs, so
+// every step of the inverse is one FP32x2 instruction for both blocks on the
+// FMA pipe (the packed integer kernels keep the ALU pipe the busier one).
+// Exact: every value is a multiple of 1/64 below 2^17 in magnitude (24-bit
+// significand), so no add or fused multiply-add ever rounds.
+//   * dequantisation folds into the column inverse: each butterfly add
+//     X_a +- X_b becomes FFMA2(q_b, +-k_b, X_a) with k = Q' E / 64 (the
+//     column's DC term is one FMUL2/FFMA2), so the inverse yields x_hat - 128
+//     directly; + 128.5 rides on W[0][0] (the all-ones basis image).
+//   * output: add.rm.f32x2 with 1.5 * 2^23 + 32768 floors to the integer grid,
+//     so the low 16 bits of each lane are 32768 + floor(x_hat + 0.5); PRMT
+//     pairs two lanes, VIADDMNMX.S16x2.RELU clamps both to [0, 255], PRMT
+//     gathers the bytes.
+// Rows 0-3 of the column pass stay in registers, rows 4-7 wait in shared
+// memory (as 64-bit pairs); the original pixels wait there too for the SSE.
+// pos[p].x = r (float bits), pos[p].y = k = Q' E / 64 (float bits).
+// ---------------------------------------------------------------------------
+struct F2 {  // two fp32 lanes (block A, block B) in one 64-bit register pair
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 f2_splat(float a) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r.v) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) {
+  F2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_fma(F2 a, float k, F2 c) {  // a * k + c, k shared by both lanes
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(f2_splat(k).v), "l"(c.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_mul(F2 a, float k) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(f2_splat(k).v));
+  return r;
+}
+
+// q (exact, as floats) of one coefficient position for both blocks from the
+// biased linear form zb (see quant_lanes_f); `magic` = {M, M}.
+__device__ __forceinline__ F2 quant_q2(u32 zb, float r, F2 magic) {
+  F2 F, Zf, Q;
+  const u32 fa = __byte_perm(zb, 0x4B000000u, 0x7610);
+  const u32 fb = __byte_perm(zb, 0x4B000000u, 0x7632);
+  asm("mov.b64 %0, {%1, %2};" : "=l"(F.v) : "r"(fa), "r"(fb));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(Zf.v) : "l"(F.v), "l"(kQfOffset));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(Q.v) : "l"(Zf.v), "l"(f2_splat(r).v), "l"(magic.v));
+  return Q - magic;
+}
+
+// Column inverse x = T^T (k o q) with the dequantisation folded into the
+// butterfly (inv8's graph; each X_u, u > 0, enters one add and one subtract).
+template <bool DC>
+__device__ __forceinline__ void inv8_dq(const F2 (&q)[8], const float (&k)[8], F2 dc, F2 (&x)[8]) {
+  const F2 X0 = DC ? f2_fma(q[0], k[0], dc) : f2_mul(q[0], k[0]);
+  const F2 b0 = f2_fma(q[4], k[4], X0), b1 = f2_fma(q[4], -k[4], X0);
+  const F2 a0 = f2_fma(q[2], k[2], b0), a3 = f2_fma(q[2], -k[2], b0);
+  const F2 a1 = f2_fma(q[6], -k[6], b1), a2 = f2_fma(q[6], k[6], b1);
+  x[0] = f2_fma(q[1], k[1], a0);
+  x[7] = f2_fma(q[1], -k[1], a0);
+  x[1] = f2_fma(q[5], -k[5], a1);
+  x[6] = f2_fma(q[5], k[5], a1);
+  x[2] = f2_fma(q[3], -k[3], a2);
+  x[5] = f2_fma(q[3], k[3], a2);
+  x[3] = f2_fma(q[7], -k[7], a3);
+  x[4] = f2_fma(q[7], k[7], a3);
+}
+
+// One reconstructed row of both blocks (y = x_hat + 0.5 per lane) -> bytes.
+constexpr u32 kFiFloorMagic = 0x4B408000u;  // 1.5 * 2^23 + 32768
+__device__ __forceinline__ uint4 pack_row_f(const F2 (&y)[8]) {
+  u32 lo[8], hi[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    unsigned long long t;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y[j].v), "l"(f2_splat(__uint_as_float(kFiFloorMagic)).v));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo[j]), "=r"(hi[j]) : "l"(t));
+  }
+  u32 ha[4], hb[4];  // 16-bit fields 32768 + floor -> clamped pixels
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ha[j] = __viaddmin_s16x2_relu(__byte_perm(lo[2 * j], lo[2 * j + 1], 0x5410), 0x80008000u, 0x00FF00FFu);
+    hb[j] = __viaddmin_s16x2_relu(__byte_perm(hi[2 * j], hi[2 * j + 1], 0x5410), 0x80008000u, 0x00FF00FFu);
+  }
+  return make_uint4(__byte_perm(ha[0], ha[1], 0x6420), __byte_perm(ha[2], ha[3], 0x6420),
+                    __byte_perm(hb[0], hb[1], 0x6420), __byte_perm(hb[2], hb[3], 0x6420));
+}
+
+constexpr unsigned long long kFiSmem = 8ull * kThreads * sizeof(uint4) + 32ull * kThreads * sizeof(unsigned long long);
+
+template <class TAB = ParamTab>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_quant_fi(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
+  extern __shared__ uint4 s_dyn[];
+  uint4* s_orig = s_dyn;                                                            // [8][kThreads]
+  F2* s_park = reinterpret_cast<F2*>(s_dyn + 8 * kThreads);                         // [4 rows][8 cols][kThreads]
+  const F2 magic{qf_magic<true>(ps.n_planes)};
+  UnitLoc L;
+  u32 acc = 0;
+  if (locate_unit<true>(ps, L)) {
+    uint4 w[8];
+    load_unit<true>(L.src, L.width, w);
+    u32 x[8][8];
+    unpack_unit(w, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s_orig[i * kThreads + threadIdx.x] = w[i];
+    F2 c[4][8];
+    {
+      u32 t[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+      const F2 dc = f2_splat(128.5f);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        u32 col[8], Zc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
+        fwd8(col, Zc);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) Zc[u] += kQfBias;
+        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
+        F2 qv[8], cc[8];
+        float k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 cst = TAB::pos(q, u * 8 + v);
+          qv[u] = quant_q2(Zc[u], __uint_as_float(cst.x), magic);
+          k[u] = __uint_as_float(cst.y);
+        }
+        if (v == 0)
+          inv8_dq<true>(qv, k, dc, cc);
+        else
+          inv8_dq<false>(qv, k, dc, cc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[i][v] = cc[i];
+#pragma unroll
+        for (int i = 4; i < 8; ++i) s_park[((i - 4) * 8 + v) * kThreads + threadIdx.x] = cc[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      F2 row[8], y[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) row[v] = i < 4 ? c[i & 3][v] : s_park[((i - 4) * 8 + v) * kThreads + threadIdx.x];
+      inv8(row, y);
+      const uint4 o = pack_row_f(y);
+      if (L.dst != nullptr) st_stream16(L.dst + (int64_t)i * L.width, o);
+      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      acc = sse4(wi.x, o.x, acc);
+      acc = sse4(wi.y, o.y, acc);
+      acc = sse4(wi.z, o.z, acc);
+      acc = sse4(wi.w, o.w, acc);
+    }
+  }
+  if (sse != nullptr) block_add_u32(acc, sse + L.frame * ps.n_planes + L.plane);
+}
+
+// ---------------------------------------------------------------------------
 // K7: retain-r sweep — one read and one forward per unit, then for every r in
 // [r_min, r_max] the masked inverse, rounding and SSE, all from registers
 // (replaces the per-r reconstruct_image + mse loop, cli.py:105-113).

@@ -208,6 +208,44 @@ QParamsDev to_qparams_f(const adct_qtab_t& t, bool scalar) {
   return q;
 }
 
+// Float-pair inverse (k_quant_fi): pos.x = r (float bits), pos.y = Q' E / 64
+// (float bits; exact: Q' E < 2^24).
+QParamsDev to_qparams_fi(const adct_qtab_t& t) {
+  QParamsDev q;
+  std::memset(&q, 0, sizeof q);
+  for (int p = 0; p < 64; ++p) {
+    const float k = (float)t.qe[p] / 64.0f;
+    uint32_t kb;
+    std::memcpy(&kb, &k, sizeof kb);
+    q.pos[p].x = t.recip_f[p];
+    q.pos[p].y = kb;
+  }
+  return q;
+}
+
+// k_quant_fi is exact when every partial sum of the inverse, in units of
+// 1/64, stays below 2^24: they are bounded by sum_uv |W_uv| <=
+// sum_uv (|Z_uv| + Q'_uv / 2) E_uv <= 64 * 8192 + sum_uv qe_uv / 2
+// (|Z_uv| E_uv <= 128 n_u n_v * 64 / (n_u n_v) = 8192).
+bool fi_exact(const adct_qtab_t& t) {
+  double s = 64.0 * 8192.0;
+  for (int p = 0; p < 64; ++p) s += 0.5 * (double)t.qe[p];
+  return s < 16777216.0;
+}
+
+// ADCT_FI_KERNEL: "wide" (default) runs k_quant_fi for coarse tables (the
+// 16-bit-lane kernels cannot hold their reconstruction), "all" for every
+// paired table, "off" keeps k_quant_hybrid (A/B).
+int fi_kernel_choice() {
+  static const int v = [] {
+    const char* e = std::getenv("ADCT_FI_KERNEL");
+    if (e && std::strcmp(e, "off") == 0) return 0;
+    if (e && std::strcmp(e, "all") == 0) return 2;
+    return 1;
+  }();
+  return v;
+}
+
 // ADCT_QUANT_FLOAT = 0 selects the integer (multiply-high) quantiser (A/B).
 int quant_float_choice() {
   static const int v = [] {
@@ -592,6 +630,31 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
   const size_t nsse = (size_t)n_frames * n_planes;
   if (sse && nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
   u64* d_sse = reinterpret_cast<u64*>(sse);
+  if (qf && quant_kernel_choice() == 1 && fi_exact(*qtab) &&
+      (fi_kernel_choice() == 2 || (wide && fi_kernel_choice() == 1))) {
+    PlaneSetHost pf;  // two blocks per thread where every plane pairs
+    rc = build_planes(planes, n_planes, n_frames, pf, false);
+    if (rc != ADCT_OK) return rc;
+    if (pf.pair) {
+      QParamsDev qi = to_qparams_fi(*qtab);
+      if (void* jf = jit::quant_function(jit::kFloatInv, qi, s)) {  // table-specialised build
+        void* args[] = {&pf.dev, &qi, &d_sse};
+        int rcj = ADCT_OK;
+        const int rcc = for_frame_chunks(pf, n_frames, [&](dim3 g) {
+          if (const int cr = jit::launch(jf, g, dim3(kThreads), kFiSmem, s, args)) {
+            g_last_cuda = cr;
+            rcj = ADCT_ERR_CUDA;
+          }
+        });
+        return rcj != ADCT_OK ? rcj : rcc;
+      }
+      ADCT_CUDA_TRY(
+          cudaFuncSetAttribute(k_quant_fi<ParamTab>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFiSmem));
+      return for_frame_chunks(pf, n_frames, [&](dim3 g) {
+        k_quant_fi<ParamTab><<<g, kThreads, kFiSmem, s>>>(pf.dev, qi, d_sse);
+      });
+    }
+  }
   if (wide) {
     QParamsDev qh;
     if (wide_kernel_choice() == 1 && (qf ? (qh = to_qparams_f(*qtab, true), true) : to_qparams_hybrid(*qtab, &qh))) {

@@ -7,7 +7,11 @@ q = int(sys.argv[1]); qf = sys.argv[2] == "1"; kern = sys.argv[3] if len(sys.arg
 t = quant.quant_table(q)
 M = 0xFFFFFFFF
 qe = [t.qe[p] for p in range(64)]
-if qf:
+if kern == "fi":
+    import struct
+    pos = [(t.recip_f[p], struct.unpack("<I", struct.pack("<f", qe[p] / 64.0))[0], 0, 0) for p in range(64)]
+    wadd = [0] * 64
+elif qf:
     pos = [(t.recip_f[p], 0, 0, qe[p] & M) for p in range(64)]
     wadd = [((-0x4B400000 * qe[p]) & M) if kern != "p" else 0 for p in range(64)]
     wadd[0] = (wadd[0] + (((24576 if t.aligned else 32768) + 32) * 65537 if kern == "p" else 32 + 8192)) & M
@@ -26,6 +30,7 @@ prog = ctypes.c_void_p()
 L.nvrtcCreateProgram(ctypes.byref(prog), src, b"x.cu", 2, (ctypes.c_char_p * 2)(d, k), (ctypes.c_char_p * 2)(b"adct_device.cuh", b"adct_kernels.cuh"))
 al = "false" if t.aligned else "true"
 e = (f"adct::k_quant_p<true, {al}, BakedTab, {'true' if qf else 'false'}>" if kern == "p"
+     else "adct::k_quant_fi<BakedTab>" if kern == "fi"
      else f"adct::k_quant_hybrid<BakedTab, {'true' if qf else 'false'}>").encode()
 L.nvrtcAddNameExpression(prog, e)
 opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-Xptxas=-v"]
