@@ -592,66 +592,112 @@ __device__ __forceinline__ uint4 pack_row_f(const F2 (&y)[8]) {
                     __byte_perm(hb[0], hb[1], 0x6420), __byte_perm(hb[2], hb[3], 0x6420));
 }
 
-constexpr unsigned long long kFiSmem = 8ull * kThreads * sizeof(uint4) + 32ull * kThreads * sizeof(unsigned long long);
+__device__ __forceinline__ u32 f2_lo(F2 a) { return (u32)a.v; }
+__device__ __forceinline__ u32 f2_hi(F2 a) { return (u32)(a.v >> 32); }
+__device__ __forceinline__ F2 f2_make(u32 lo, u32 hi) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "r"(lo), "r"(hi));
+  return r;
+}
 
-template <class TAB = ParamTab>
-__global__ void __launch_bounds__(kThreads, 2)
+// Forward, quantiser and column inverse of one unit (rows w).  Rows 0-3 of the
+// column-pass result stay in c; rows 4-7 go to the park, two columns per
+// 16-byte slot: park(r, j) is this thread's slot for row 4 + r, columns 2j, 2j+1.
+template <class TAB, class PARK>
+__device__ __forceinline__ void fi_columns(const uint4 (&w)[8], const QParamsDev& q, F2 magic, F2 (&c)[4][8],
+                                           PARK park) {
+  u32 x[8][8], t[8][8];
+  unpack_unit(w, x);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
+  const F2 dc = f2_splat(128.5f);
+#pragma unroll
+  for (int v = 0; v < 8; v += 2) {
+    F2 hold[4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int vv = v + h;
+      u32 col[8], Zc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) col[i] = t[i][vv];
+      fwd8(col, Zc);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Zc[u] += kQfBias;
+      if (vv == 0) Zc[0] -= 8192u * 65537u;  // level shift
+      F2 qv[8], cc[8];
+      float k[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 cst = TAB::pos(q, u * 8 + vv);
+        qv[u] = quant_q2(Zc[u], __uint_as_float(cst.x), magic);
+        k[u] = __uint_as_float(cst.y);
+      }
+      if (vv == 0)
+        inv8_dq<true>(qv, k, dc, cc);
+      else
+        inv8_dq<false>(qv, k, dc, cc);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i][vv] = cc[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (h == 0)
+          hold[i] = cc[4 + i];
+        else
+          park(i, v >> 1) = make_uint4(f2_lo(hold[i]), f2_hi(hold[i]), f2_lo(cc[4 + i]), f2_hi(cc[4 + i]));
+      }
+    }
+  }
+}
+
+// Row pass of row i -> packed bytes; `c` rows 0-3, park for rows 4-7.
+template <class PARK>
+__device__ __forceinline__ uint4 fi_row(int i, const F2 (&c)[4][8], PARK park) {
+  F2 row[8], y[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (i < 4) {
+      row[2 * j] = c[i & 3][2 * j];
+      row[2 * j + 1] = c[i & 3][2 * j + 1];
+    } else {
+      const uint4 s = park(i - 4, j);
+      row[2 * j] = f2_make(s.x, s.y);
+      row[2 * j + 1] = f2_make(s.z, s.w);
+    }
+  }
+  inv8(row, y);
+  return pack_row_f(y);
+}
+
+// Shared memory per thread: 8 slots of original rows + 16 park slots.  CTAs
+// of kFiThreads units (128: 4 CTAs per SM at 48 KB each, so one CTA's load
+// phase overlaps the others' arithmetic).
+constexpr int kFiThreads = 128;
+__host__ __device__ constexpr unsigned long long fi_smem(int nt) { return 24ull * nt * sizeof(uint4); }
+constexpr unsigned long long kFiSmem = fi_smem(kFiThreads);
+
+template <class TAB = ParamTab, int NT = kFiThreads>
+__global__ void __launch_bounds__(NT, 512 / NT)
     k_quant_fi(PlaneSetDev ps, const __grid_constant__ QParamsDev q, u64* __restrict__ sse) {
   extern __shared__ uint4 s_dyn[];
-  uint4* s_orig = s_dyn;                                                            // [8][kThreads]
-  F2* s_park = reinterpret_cast<F2*>(s_dyn + 8 * kThreads);                         // [4 rows][8 cols][kThreads]
+  uint4* const sm = s_dyn + threadIdx.x;  // slot k of this thread: sm[k * NT]
+  auto park = [sm](int r, int j) -> uint4& { return sm[(8 + r * 4 + j) * NT]; };
   const F2 magic{qf_magic<true>(ps.n_planes)};
   UnitLoc L;
   u32 acc = 0;
-  if (locate_unit<true>(ps, L)) {
-    uint4 w[8];
-    load_unit<true>(L.src, L.width, w);
-    u32 x[8][8];
-    unpack_unit(w, x);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s_orig[i * kThreads + threadIdx.x] = w[i];
+  if (locate_unit<true, NT>(ps, L)) {
     F2 c[4][8];
     {
-      u32 t[8][8];
+      uint4 w[8];
+      load_unit<true>(L.src, L.width, w);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fwd8(x[i], t[i]);
-      const F2 dc = f2_splat(128.5f);
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        u32 col[8], Zc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) col[i] = t[i][v];
-        fwd8(col, Zc);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) Zc[u] += kQfBias;
-        if (v == 0) Zc[0] -= 8192u * 65537u;  // level shift
-        F2 qv[8], cc[8];
-        float k[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint4 cst = TAB::pos(q, u * 8 + v);
-          qv[u] = quant_q2(Zc[u], __uint_as_float(cst.x), magic);
-          k[u] = __uint_as_float(cst.y);
-        }
-        if (v == 0)
-          inv8_dq<true>(qv, k, dc, cc);
-        else
-          inv8_dq<false>(qv, k, dc, cc);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) c[i][v] = cc[i];
-#pragma unroll
-        for (int i = 4; i < 8; ++i) s_park[((i - 4) * 8 + v) * kThreads + threadIdx.x] = cc[i];
-      }
+      for (int i = 0; i < 8; ++i) sm[i * NT] = w[i];
+      fi_columns<TAB>(w, q, magic, c, park);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      F2 row[8], y[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v) row[v] = i < 4 ? c[i & 3][v] : s_park[((i - 4) * 8 + v) * kThreads + threadIdx.x];
-      inv8(row, y);
-      const uint4 o = pack_row_f(y);
+      const uint4 o = fi_row(i, c, park);
       if (L.dst != nullptr) st_stream16(L.dst + (int64_t)i * L.width, o);
-      const uint4 wi = s_orig[i * kThreads + threadIdx.x];
+      const uint4 wi = sm[i * NT];
       acc = sse4(wi.x, o.x, acc);
       acc = sse4(wi.y, o.y, acc);
       acc = sse4(wi.z, o.z, acc);

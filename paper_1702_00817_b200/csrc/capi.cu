@@ -246,6 +246,15 @@ int fi_kernel_choice() {
   return v;
 }
 
+// ADCT_FI_THREADS = 256 runs k_quant_fi with 256-unit tiles (A/B; default 128).
+int fi_threads_choice() {
+  static const int v = [] {
+    const char* e = std::getenv("ADCT_FI_THREADS");
+    return (e && std::strcmp(e, "256") == 0) ? 256 : kFiThreads;
+  }();
+  return v;
+}
+
 // ADCT_QUANT_FLOAT = 0 selects the integer (multiply-high) quantiser (A/B).
 int quant_float_choice() {
   static const int v = [] {
@@ -632,26 +641,36 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
   u64* d_sse = reinterpret_cast<u64*>(sse);
   if (qf && quant_kernel_choice() == 1 && fi_exact(*qtab) &&
       (fi_kernel_choice() == 2 || (wide && fi_kernel_choice() == 1))) {
+    const int nt = fi_threads_choice();  // units per tile = threads per CTA
     PlaneSetHost pf;  // two blocks per thread where every plane pairs
-    rc = build_planes(planes, n_planes, n_frames, pf, false);
+    rc = build_planes(planes, n_planes, n_frames, pf, false, nt);
     if (rc != ADCT_OK) return rc;
     if (pf.pair) {
       QParamsDev qi = to_qparams_fi(*qtab);
-      if (void* jf = jit::quant_function(jit::kFloatInv, qi, s)) {  // table-specialised build
+      const size_t smem = fi_smem(nt);
+      const int kind = nt == 256 ? jit::kFloatInv256 : jit::kFloatInv;
+      if (void* jf = jit::quant_function(kind, qi, s)) {  // table-specialised
         void* args[] = {&pf.dev, &qi, &d_sse};
         int rcj = ADCT_OK;
         const int rcc = for_frame_chunks(pf, n_frames, [&](dim3 g) {
-          if (const int cr = jit::launch(jf, g, dim3(kThreads), kFiSmem, s, args)) {
+          if (const int cr = jit::launch(jf, g, dim3(nt), smem, s, args)) {
             g_last_cuda = cr;
             rcj = ADCT_ERR_CUDA;
           }
         });
         return rcj != ADCT_OK ? rcj : rcc;
       }
+      if (nt == 256) {
+        ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_fi<ParamTab, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        return for_frame_chunks(pf, n_frames, [&](dim3 g) {
+          k_quant_fi<ParamTab, 256><<<g, 256, smem, s>>>(pf.dev, qi, d_sse);
+        });
+      }
       ADCT_CUDA_TRY(
-          cudaFuncSetAttribute(k_quant_fi<ParamTab>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFiSmem));
+          cudaFuncSetAttribute(k_quant_fi<ParamTab>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       return for_frame_chunks(pf, n_frames, [&](dim3 g) {
-        k_quant_fi<ParamTab><<<g, kThreads, kFiSmem, s>>>(pf.dev, qi, d_sse);
+        k_quant_fi<ParamTab><<<g, kFiThreads, smem, s>>>(pf.dev, qi, d_sse);
       });
     }
   }

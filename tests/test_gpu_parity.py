@@ -224,11 +224,16 @@ def test_empty_batch(cuda):
 @pytest.mark.parametrize("env", [{"ADCT_QUANT_KERNEL": "grid"}, {"ADCT_WIDE_KERNEL": "scalar"},
                                  {"ADCT_PIPELINE_DEPTH": "2"}, {"ADCT_QUANT_FLOAT": "0"},
                                  {"ADCT_QUANT_FLOAT": "0", "ADCT_WIDE_KERNEL": "scalar"},
-                                 {"ADCT_PIPELINE_THREADS": "1"}, {"ADCT_QUANT_JIT_AFTER": "1"}])
+                                 {"ADCT_PIPELINE_THREADS": "1"}, {"ADCT_QUANT_JIT_AFTER": "1"},
+                                 {"ADCT_FI_KERNEL": "all"}, {"ADCT_FI_KERNEL": "all", "ADCT_QUANT_JIT_AFTER": "1"},
+                                 {"ADCT_FI_KERNEL": "all", "ADCT_FI_THREADS": "256"},
+                                 {"ADCT_FI_KERNEL": "off"}])
 def test_alternate_kernel_paths(cuda, env):
     """The A/B switches keep their kernels exact: one-tile-per-CTA quant
-    kernel, scalar coarse-table kernel, a 2-deep host pipeline (child process:
-    the switches are read once per process)."""
+    kernel, scalar coarse-table kernel, the float-pair-inverse kernel for every
+    table (generic and table-specialised, both tile sizes) or for none (the
+    32-bit hybrid), a 2-deep host pipeline (child process: the switches are
+    read once per process)."""
     import os
     import subprocess
     import sys

@@ -7,7 +7,7 @@ q = int(sys.argv[1]); qf = sys.argv[2] == "1"; kern = sys.argv[3] if len(sys.arg
 t = quant.quant_table(q)
 M = 0xFFFFFFFF
 qe = [t.qe[p] for p in range(64)]
-if kern == "fi":
+if kern in ("fi", "fip"):
     import struct
     pos = [(t.recip_f[p], struct.unpack("<I", struct.pack("<f", qe[p] / 64.0))[0], 0, 0) for p in range(64)]
     wadd = [0] * 64
@@ -31,6 +31,7 @@ L.nvrtcCreateProgram(ctypes.byref(prog), src, b"x.cu", 2, (ctypes.c_char_p * 2)(
 al = "false" if t.aligned else "true"
 e = (f"adct::k_quant_p<true, {al}, BakedTab, {'true' if qf else 'false'}>" if kern == "p"
      else "adct::k_quant_fi<BakedTab>" if kern == "fi"
+     else "adct::k_quant_fip<BakedTab>" if kern == "fip"
      else f"adct::k_quant_hybrid<BakedTab, {'true' if qf else 'false'}>").encode()
 L.nvrtcAddNameExpression(prog, e)
 opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-Xptxas=-v"]
