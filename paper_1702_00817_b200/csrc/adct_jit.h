@@ -9,9 +9,7 @@ namespace jit {
 
 enum Kind { kQuantPairAligned = 0, kQuantPairFlip = 1, kQuantSingleAligned = 2, kQuantSingleFlip = 3, kHybrid = 4,
             kFloatOffset = 5,  // + kind: the float-quantiser (QF) variant
-            kHybridF = kHybrid + kFloatOffset,
-            kFloatInv = 16,    // k_quant_fi
-            kFloatInv256 = 17 };  // k_quant_fi with 256-unit tiles
+            kHybridF = kHybrid + kFloatOffset };
 
 // The specialised kernel for (kind, table) once the table has been used often
 // enough and compiled; nullptr while the generic kernel should run.

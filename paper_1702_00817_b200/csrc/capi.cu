@@ -648,18 +648,9 @@ static int quant_planes(const adct_plane_t* planes, int32_t n_planes, int64_t n_
     if (pf.pair) {
       QParamsDev qi = to_qparams_fi(*qtab);
       const size_t smem = fi_smem(nt);
-      const int kind = nt == 256 ? jit::kFloatInv256 : jit::kFloatInv;
-      if (void* jf = jit::quant_function(kind, qi, s)) {  // table-specialised
-        void* args[] = {&pf.dev, &qi, &d_sse};
-        int rcj = ADCT_OK;
-        const int rcc = for_frame_chunks(pf, n_frames, [&](dim3 g) {
-          if (const int cr = jit::launch(jf, g, dim3(nt), smem, s, args)) {
-            g_last_cuda = cr;
-            rcj = ADCT_ERR_CUDA;
-          }
-        });
-        return rcj != ADCT_OK ? rcj : rcc;
-      }
+      // no run-time table specialisation here: with the constants as
+      // immediates this kernel measured 2.3 % slower (ptxas already feeds them
+      // to the FP32x2 instructions from the constant bank)
       if (nt == 256) {
         ADCT_CUDA_TRY(cudaFuncSetAttribute(k_quant_fi<ParamTab, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));

@@ -142,8 +142,6 @@ const char* kernel_expression(int kind) {
     case kQuantSingleAligned + kFloatOffset: return "adct::k_quant_p<false, false, BakedTab, true>";
     case kQuantSingleFlip + kFloatOffset: return "adct::k_quant_p<false, true, BakedTab, true>";
     case kHybridF: return "adct::k_quant_hybrid<BakedTab, true>";
-    case kFloatInv: return "adct::k_quant_fi<BakedTab>";
-    case kFloatInv256: return "adct::k_quant_fi<BakedTab, 256>";
     default: return nullptr;
   }
 }
@@ -200,10 +198,7 @@ CUfunction build(int kind, const QParamsDev& q) {
   CUmodule mod = nullptr;
   if (good) good = dr.load(&mod, cubin.data()) == CUDA_SUCCESS;  // module lives for the process
   if (good) good = dr.get_function(&fn, mod, lowered) == CUDA_SUCCESS;
-  const int smem = (kind == kHybrid || kind == kHybridF) ? (int)kHybridSmem
-                   : kind == kFloatInv                   ? (int)kFiSmem
-                   : kind == kFloatInv256                ? (int)fi_smem(256)
-                                                         : (int)(2 * 8 * kThreads * sizeof(uint4));
+  const int smem = (kind == kHybrid || kind == kHybridF) ? (int)kHybridSmem : (int)(2 * 8 * kThreads * sizeof(uint4));
   if (good)
     good = dr.set_attribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) == CUDA_SUCCESS;
   nv.destroy(&prog);

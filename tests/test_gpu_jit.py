@@ -56,8 +56,8 @@ def _run(after):
 def test_specialised_kernels_are_exact():
     compiled, launches, failures = _run(1)
     assert failures == 0
-    assert compiled >= 6  # pair/single x aligned/flip, hybrid, the custom table's kernel
-    assert launches >= 12
+    assert compiled >= 4  # pair/single x aligned/flip (coarse tables run k_quant_fi, never specialised)
+    assert launches >= 9  # 4 tables x 2 calls + the planes call
 
 
 def test_specialisation_off():
