@@ -7,7 +7,9 @@ compute path: a missing library or GPU raises.
 
 Routing:
 * `forward_2d_unscaled` on 8-bit-range integers -> K1 exact integer kernel;
-  any other real input -> the float64 flow-graph kernel without scaling.
+  any other real input -> the dense float64 kernel with K (exact for
+  integers).  Device tensors choose by dtype (uint8), never by scanning
+  values, so no call synchronises the host with the GPU.
 * `forward_2d`, `inverse_2d`, `coefficient_blocks`, `reconstruct_image`,
   `compress_image` keep the reference's float64 semantics (unrounded,
   clamped) -> float64 flow-graph kernels (agree with the reference's dense
@@ -126,12 +128,12 @@ def _matrix(t) -> np.ndarray:
 
 
 def _is_u8_range_integral(a) -> bool:
+    """Whether `a` can take the exact 8-bit integer kernel.  Device tensors
+    decide by dtype alone (a value scan would be a device-wide reduction and a
+    host sync on every call); other device dtypes take the dense float64
+    kernel, exact for integer values.  Host arrays are scanned on the host."""
     if isinstance(a, torch.Tensor):
-        if a.dtype == torch.uint8:
-            return True
-        if a.dtype.is_floating_point:
-            return bool(((a == a.round()) & (a >= 0) & (a <= 255)).all())
-        return bool(((a >= 0) & (a <= 255)).all())
+        return a.dtype == torch.uint8
     a = np.asarray(a)
     if a.dtype == np.uint8:
         return True
@@ -162,37 +164,23 @@ def forward_2d(t, block):
 
 
 def forward_2d_unscaled(t, block):
-    """K B K^T without the diagonal scaling (codec.py:74-81); integer-exact."""
+    """K B K^T without the diagonal scaling (codec.py:74-81); integer-exact.
+    8-bit integer blocks of the proposed kernel take K1 (exact integer
+    flow graph); anything else the dense float64 kernel with K itself (exact
+    for integer values, the reference's own product otherwise)."""
     integral_in = (block.dtype.kind in "iub") if not isinstance(block, torch.Tensor) else not block.dtype.is_floating_point
-    if not is_proposed(t):
-        k = np.asarray(t.kernel.entries, dtype=np.float64)
-        x, was_np = _to_dev(block, torch.float64)
-        xs, lead = _blocks_as_images(x)
-        z = batch.forward_dense(xs, k)
-        z = z.reshape(*lead, 8, 8) if lead else z.reshape(8, 8)
-        return _back(torch.round(z).to(torch.int64) if integral_in else z, was_np)
-    if _is_u8_range_integral(block):
+    if is_proposed(t) and _is_u8_range_integral(block):
         x, was_np = _to_dev(block, torch.uint8)
         xs, lead = _blocks_as_images(x)
         z = batch.forward_int(xs).reshape(*lead, 8, 8) if lead else batch.forward_int(xs).reshape(8, 8)
         z = z.to(torch.int64) if integral_in else z.to(torch.float64)
         return _back(z, was_np)
+    k = np.asarray(t.kernel.entries, dtype=np.float64)
     x, was_np = _to_dev(block, torch.float64)
     xs, lead = _blocks_as_images(x)
-    d = torch.as_tensor(_d_outer(), device=xs.device)
-    z = batch.forward_f64(xs) / d  # undo the float64 scaling exactly enough for integers < 2^40
+    z = batch.forward_dense(xs, k)
     z = z.reshape(*lead, 8, 8) if lead else z.reshape(8, 8)
-    if integral_in:
-        z = torch.round(z).to(torch.int64)
-    return _back(z, was_np)
-
-
-@lru_cache(maxsize=1)
-def _d_outer() -> np.ndarray:
-    from .transforms import proposed_scaling
-
-    d = proposed_scaling().diag
-    return np.outer(d, d)
+    return _back(torch.round(z).to(torch.int64) if integral_in else z, was_np)
 
 
 def inverse_2d(t, coeffs):

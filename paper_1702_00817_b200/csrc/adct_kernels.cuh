@@ -1061,60 +1061,109 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------------------
 // Float64 transforms (real-valued inputs; signature parity with the
-// reference's float API).  One thread per 8x8 block.
+// reference's float API).  Eight threads per 8x8 block, one block row each
+// (a warp holds 4 blocks): a thread loads / stores one contiguous 8-value row
+// (the 8 threads of a block cover the block's 512 coefficient bytes, a warp
+// 2 KB contiguous), runs the 1-D transform on it, and the row <-> column
+// turns go through a padded per-warp shared-memory tile (xpose8).  Register
+// footprint is 8 values per thread instead of a whole block, so nothing
+// spills and 2 CTAs of 256 threads x 8 warps stay resident per SM.
 // ---------------------------------------------------------------------------
+constexpr int kRowThreads = 256;               // threads per CTA: 32 blocks
+constexpr int kRowBlocks = kRowThreads / 8;    // blocks per CTA
+constexpr int kXposeWarp = 4 * 8 * 9;          // doubles per warp tile (4 blocks x 8 rows, padded to 9)
+
 __device__ __forceinline__ double dscale(int u) {
   // d = (1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2, 1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2), kernels.py:149-157
   return (u & 1) ? 0.70710678118654757 : ((u & 2) ? 0.5 : 0.35355339059327379);
 }
 
-__global__ void __launch_bounds__(kThreads)
-    k_forward_f64(const double* __restrict__ img, int h, int w, int64_t nblocks,
-                  double* __restrict__ coef) {
-  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (blk >= nblocks) return;
-  const int64_t frame = blockIdx.y;
-  const int nbc = w / 8;
-  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
-  const double* src = img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
-  double x[8][8], Z[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[i][j] = src[(int64_t)i * w + j];
-  fwd2d(x, Z);
-  double* dst = coef + (frame * nblocks + blk) * 64;
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) dst[u * 8 + v] = Z[u][v] * (dscale(u) * dscale(v));
+// This thread's block and row.  `buf` = the warp's transpose tile.
+struct RowLoc {
+  int64_t blk;  // block index within the frame
+  int64_t frame;
+  int i;        // row of the block this thread owns
+  int g;        // block slot within the warp (0..3)
+  bool active;
+  double* buf;
+};
+
+__device__ __forceinline__ RowLoc row_locate(int64_t nblocks, double* tiles) {
+  RowLoc L;
+  L.blk = (int64_t)blockIdx.x * kRowBlocks + (threadIdx.x >> 3);
+  L.frame = blockIdx.y;
+  L.i = threadIdx.x & 7;
+  L.g = (threadIdx.x >> 3) & 3;
+  L.active = L.blk < nblocks;
+  L.buf = tiles + (threadIdx.x >> 5) * kXposeWarp;
+  return L;
 }
 
-__global__ void __launch_bounds__(kThreads)
+// Row <-> column turn within each block: thread i of block g gives in[v]
+// (its row) and gets out[u] = in[i] of thread u.  The 9-double row pitch
+// keeps both the stores and the strided loads free of bank conflicts.
+__device__ __forceinline__ void xpose8(const RowLoc& L, const double (&in)[8], double (&out)[8]) {
+#pragma unroll
+  for (int v = 0; v < 8; ++v) L.buf[(L.g * 8 + L.i) * 9 + v] = in[v];
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) out[u] = L.buf[(L.g * 8 + u) * 9 + L.i];
+  __syncwarp();
+}
+
+__device__ __forceinline__ const double* image_row(const double* img, const RowLoc& L, int h, int w, int64_t nbc) {
+  const int64_t brow = L.blk / nbc, bcol = L.blk - brow * nbc;
+  return img + L.frame * (int64_t)h * w + (brow * 8 + L.i) * w + bcol * 8;
+}
+
+__global__ void __launch_bounds__(kRowThreads)
+    k_forward_f64(const double* __restrict__ img, int h, int w, int64_t nblocks,
+                  double* __restrict__ coef) {
+  __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
+  const RowLoc L = row_locate(nblocks, tiles);
+  double x[8], t[8], c[8], Z[8];
+  if (L.active) {
+    const double* src = image_row(img, L, h, w, w / 8);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = src[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = 0.0;
+  }
+  fwd8(x, t);        // row i: t[i][v] = (T x_i)[v]
+  xpose8(L, t, c);   // column i: c[u'] = t[u'][i]
+  fwd8(c, Z);        // Z[u][i]
+#pragma unroll
+  for (int u = 0; u < 8; ++u) Z[u] *= dscale(u) * dscale(L.i);
+  xpose8(L, Z, t);   // row i of the scaled coefficients
+  if (!L.active) return;
+  double* dst = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) dst[v] = t[v];
+}
+
+__global__ void __launch_bounds__(kRowThreads)
     k_inverse_f64(const double* __restrict__ coef, int h, int w, int64_t nblocks, int r,
                   int clamp, double* __restrict__ out) {
-  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (blk >= nblocks) return;
-  const int64_t frame = blockIdx.y;
-  const int nbc = w / 8;
-  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
-  const double* src = coef + (frame * nblocks + blk) * 64;
-  double W[8][8], x[8][8];
+  __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
+  const RowLoc L = row_locate(nblocks, tiles);
+  double W[8], c[8], col[8], x[8];
+  if (L.active) {
+    const double* src = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+    for (int v = 0; v < 8; ++v) W[v] = (zz_rank(L.i, v) < r) ? src[v] * (dscale(L.i) * dscale(v)) : 0.0;
+  } else {
 #pragma unroll
-    for (int v = 0; v < 8; ++v)
-      W[u][v] = (zz_rank(u, v) < r) ? src[u * 8 + v] * (dscale(u) * dscale(v)) : 0.0;
-  inv2d(W, x);
-  double* dst = out + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
+    for (int v = 0; v < 8; ++v) W[v] = 0.0;
+  }
+  inv8(W, c);          // row u = i: c[u][j] = (T^T W_u)[j]
+  xpose8(L, c, col);   // column j = i: col[u] = c[u][i]
+  inv8(col, x);        // x[i'][j] for i' = 0..7
+  xpose8(L, x, c);     // row i of the reconstruction
+  if (!L.active) return;
+  double* dst = const_cast<double*>(image_row(out, L, h, w, w / 8));
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double v = x[i][j];
-      if (clamp) v = fmin(fmax(v, 0.0), 255.0);
-      dst[(int64_t)i * w + j] = v;
-    }
+  for (int j = 0; j < 8; ++j) dst[j] = clamp ? fmin(fmax(c[j], 0.0), 255.0) : c[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -1160,7 +1209,8 @@ __global__ void __launch_bounds__(kThreads)
 // r-sweep that reconstructs incrementally:
 //   x_hat_r = x_hat_{r-1} + Y[u][v] * C[u]^T C[v]   ((u,v) = zigzag position r-1)
 // with the clamped float64 SSE of the reference's convention per r
-// (cli.py:105-113: reconstruct_image + mse).
+// (cli.py:105-113: reconstruct_image + mse).  Same row-per-thread layout as
+// the float64 flow-graph kernels above.
 // ---------------------------------------------------------------------------
 struct DenseMat {
   double c[64];  // row-major C[u][k]
@@ -1187,151 +1237,123 @@ __device__ __forceinline__ void dense8t(const DenseMat& M, const double (&y)[8],
 }
 
 template <typename InT>
-__device__ __forceinline__ void load_block_f64(const InT* src, int w, double (&x)[8][8]) {
+__device__ __forceinline__ void load_row_f64(const InT* img, const RowLoc& L, int h, int w, double (&x)[8]) {
+  if (!L.active) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) x[j] = 0.0;
+    return;
+  }
+  const int64_t nbc = w / 8, brow = L.blk / nbc, bcol = L.blk - brow * nbc;
+  const InT* src = img + L.frame * (int64_t)h * w + (brow * 8 + L.i) * w + bcol * 8;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[i][j] = (double)src[(int64_t)i * w + j];
+  for (int j = 0; j < 8; ++j) x[j] = (double)src[j];
 }
 
-// Y = C X C^T: rows then columns.
-__device__ __forceinline__ void dense_fwd2d(const DenseMat& M, const double (&x)[8][8], double (&Y)[8][8]) {
-  double t[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) dense8(M, x[i], t[i]);
-#pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    double col[8], out[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) col[i] = t[i][v];
-    dense8(M, col, out);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) Y[u][v] = out[u];
-  }
+// Column i of Y = C X C^T for this thread's block (Yc[u] = Y[u][i]).
+__device__ __forceinline__ void dense_fwd_cols(const DenseMat& M, const RowLoc& L, const double (&x)[8],
+                                               double (&Yc)[8]) {
+  double t[8], c[8];
+  dense8(M, x, t);   // row i: t[i][v] = (C x_i)[v]
+  xpose8(L, t, c);   // column i: c[i'] = t[i'][i]
+  dense8(M, c, Yc);  // Y[u][i]
 }
 
 template <typename InT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kRowThreads)
     k_dense_forward(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M,
                     double* __restrict__ coef) {
-  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (blk >= nblocks) return;
-  const int64_t frame = blockIdx.y;
-  const int nbc = w / 8;
-  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
-  double x[8][8], Y[8][8];
-  load_block_f64(img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8, w, x);
-  dense_fwd2d(M, x, Y);
-  double* dst = coef + (frame * nblocks + blk) * 64;
+  __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
+  const RowLoc L = row_locate(nblocks, tiles);
+  double x[8], Yc[8], Yr[8];
+  load_row_f64(img, L, h, w, x);
+  dense_fwd_cols(M, L, x, Yc);
+  xpose8(L, Yc, Yr);  // row i of Y
+  if (!L.active) return;
+  double* dst = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) dst[u * 8 + v] = Y[u][v];
+  for (int v = 0; v < 8; ++v) dst[v] = Yr[v];
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kRowThreads)
     k_dense_inverse(const double* __restrict__ coef, int h, int w, int64_t nblocks, int r, int clamp,
                     const DenseMat M, double* __restrict__ out) {
-  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (blk >= nblocks) return;
-  const int64_t frame = blockIdx.y;
-  const int nbc = w / 8;
-  const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
-  const double* src = coef + (frame * nblocks + blk) * 64;
-  double Y[8][8], c[8][8];
+  __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
+  const RowLoc L = row_locate(nblocks, tiles);
+  double Y[8], c[8], col[8], x[8];
+  if (L.active) {
+    const double* src = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) Y[u][v] = (zz_rank(u, v) < r) ? src[u * 8 + v] : 0.0;
-  // columns: c[:, v] = C^T Y[:, v]; rows: x[i, :] = C^T c[i, :]
-#pragma unroll
-  for (int v = 0; v < 8; ++v) {
-    double col[8], o[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) col[u] = Y[u][v];
-    dense8t(M, col, o);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c[i][v] = o[i];
-  }
-  double* dst = out + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double o[8];
-    dense8t(M, c[i], o);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) dst[(int64_t)i * w + j] = clamp ? fmin(fmax(o[j], 0.0), 255.0) : o[j];
-  }
-}
-
-// One thread per block; per r a block-wide float64 sum and one atomic per CTA.
-template <typename InT>
-__global__ void __launch_bounds__(kThreads)
-    k_dense_sweep(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M, int r_min,
-                  int r_max, double* __restrict__ sse) {
-  __shared__ double red[kThreads / 32];
-  const int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  const bool active = blk < nblocks;
-  const int64_t frame = blockIdx.y;
-  const int nbc = w / 8;
-  double x[8][8], Y[8][8], V[8][8];
-  if (active) {
-    const int brow = (int)(blk / nbc), bcol = (int)(blk % nbc);
-    load_block_f64(img + frame * (int64_t)h * w + (int64_t)brow * 8 * w + bcol * 8, w, x);
-    dense_fwd2d(M, x, Y);
+    for (int v = 0; v < 8; ++v) Y[v] = (zz_rank(L.i, v) < r) ? src[v] : 0.0;
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[i][j] = Y[i][j] = 0.0;
+    for (int v = 0; v < 8; ++v) Y[v] = 0.0;
   }
+  dense8t(M, Y, c);     // row u = i: c[u][j] = (C^T Y_u)[j]
+  xpose8(L, c, col);    // column j = i
+  dense8t(M, col, x);   // x[i'][j]
+  xpose8(L, x, c);      // row i
+  if (!L.active) return;
+  double* dst = const_cast<double*>(image_row(out, L, h, w, w / 8));
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) V[i][j] = 0.0;
+  for (int j = 0; j < 8; ++j) dst[j] = clamp ? fmin(fmax(c[j], 0.0), 255.0) : c[j];
+}
+
+// r-sweep: the block's Y waits in shared memory (read once per r at the
+// zigzag position, a broadcast within each block's 8 threads); each thread
+// updates its reconstruction row (8 FMAs per r) and adds its clamped squared
+// errors; per r a warp reduction into a per-warp shared partial, one atomic
+// per (CTA, r) at the end.
+__constant__ unsigned char kZigzagPos[64] = {
+    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,  12, 19, 26, 33, 40, 48,
+    41, 34, 27, 20, 13, 6,  7,  14, 21, 28, 35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23,
+    30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+
+template <typename InT>
+__global__ void __launch_bounds__(kRowThreads)
+    k_dense_sweep(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M, int r_min,
+                  int r_max, double* __restrict__ sse) {
+  __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
+  __shared__ double ys[kRowBlocks * 64];             // [block][u*8+v]
+  __shared__ double cs[64];                          // C
+  __shared__ double part[64][kRowThreads / 32];      // [r - r_min][warp]
+  const RowLoc L = row_locate(nblocks, tiles);
   const int nr = r_max - r_min + 1;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x < 64) cs[threadIdx.x] = M.c[threadIdx.x];
+  double x[8], Yc[8], V[8];
+  load_row_f64(img, L, h, w, x);
+  dense_fwd_cols(M, L, x, Yc);
+  double* yb = ys + (threadIdx.x >> 3) * 64;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) yb[u * 8 + L.i] = Yc[u];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) V[j] = 0.0;
+  __syncthreads();  // cs, ys
 #pragma unroll 1
   for (int k = 0; k < r_max; ++k) {
-    // zigzag position of rank k (uniform across the CTA)
-    int pos = 0;
+    const int pos = kZigzagPos[k], u = pos >> 3, v = pos & 7;
+    const double a = yb[pos] * cs[u * 8 + L.i];
 #pragma unroll
-    for (int p = 0; p < 64; ++p)
-      if (zz_rank(p >> 3, p & 7) == k) pos = p;
-    const int u = pos >> 3, v = pos & 7;
-    double y = 0.0;
-#pragma unroll
-    for (int uu = 0; uu < 8; ++uu)
-#pragma unroll
-      for (int vv = 0; vv < 8; ++vv)
-        if (uu == u && vv == v) y = Y[uu][vv];
-    double a[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = y * M.c[u * 8 + i];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) V[i][j] = fma(a[i], M.c[v * 8 + j], V[i][j]);
+    for (int j = 0; j < 8; ++j) V[j] = fma(a, cs[v * 8 + j], V[j]);
     if (k + 1 < r_min) continue;
     double acc = 0.0;
-    if (active) {
+    if (L.active) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const double d = x[i][j] - fmin(fmax(V[i][j], 0.0), 255.0);
-          acc = fma(d, d, acc);
-        }
+      for (int j = 0; j < 8; ++j) {
+        const double d = x[j] - fmin(fmax(V[j], 0.0), 255.0);
+        acc = fma(d, d, acc);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
+    if ((threadIdx.x & 31) == 0) part[k + 1 - r_min][warp] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < kThreads / 32; ++q) t += red[q];
-      atomicAdd(sse + frame * nr + (k + 1 - r_min), t);
-    }
-    __syncthreads();
+    for (int q = 0; q < kRowThreads / 32; ++q) t += part[threadIdx.x][q];
+    atomicAdd(sse + L.frame * nr + threadIdx.x, t);
   }
 }
 

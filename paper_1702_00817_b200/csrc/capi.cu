@@ -818,10 +818,10 @@ int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w, double*
   if (n == 0 || nb == 0) return ADCT_OK;
   if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
   for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
-    k_forward_f64<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(img + f0 * (int64_t)h * w, h, w, nb,
+    k_forward_f64<<<dim3(gx, (unsigned)nf), kRowThreads, 0, s>>>(img + f0 * (int64_t)h * w, h, w, nb,
                                                                coef + f0 * nb * 64);
     ADCT_CUDA_TRY(cudaGetLastError());
   }
@@ -837,10 +837,10 @@ int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w, int32_
   if (n == 0 || nb == 0) return ADCT_OK;
   if (out == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
   for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
-    k_inverse_f64<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r,
+    k_inverse_f64<<<dim3(gx, (unsigned)nf), kRowThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r,
                                                                clamp, out + f0 * (int64_t)h * w);
     ADCT_CUDA_TRY(cudaGetLastError());
   }
@@ -867,15 +867,15 @@ int adct_forward_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h
   if (n == 0 || nb == 0) return ADCT_OK;
   if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
   for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
     const dim3 g(gx, (unsigned)nf);
     if (img_is_f64)
-      k_dense_forward<double><<<g, kThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M,
+      k_dense_forward<double><<<g, kRowThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M,
                                                       coef + f0 * nb * 64);
     else
-      k_dense_forward<uint8_t><<<g, kThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
+      k_dense_forward<uint8_t><<<g, kRowThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
                                                        coef + f0 * nb * 64);
     ADCT_CUDA_TRY(cudaGetLastError());
   }
@@ -893,10 +893,10 @@ int adct_inverse_dense(const double* coef, int64_t n, int32_t h, int32_t w, cons
   if (n == 0 || nb == 0) return ADCT_OK;
   if (coef == nullptr || out == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
   for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
-    k_dense_inverse<<<dim3(gx, (unsigned)nf), kThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r, clamp, M,
+    k_dense_inverse<<<dim3(gx, (unsigned)nf), kRowThreads, 0, s>>>(coef + f0 * nb * 64, h, w, nb, r, clamp, M,
                                                                out + f0 * (int64_t)h * w);
     ADCT_CUDA_TRY(cudaGetLastError());
   }
@@ -918,15 +918,15 @@ int adct_sweep_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, 
   ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, (size_t)n * nr * sizeof(double), s));
   if (nb == 0) return ADCT_OK;
   if (img == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
-  const unsigned gx = (unsigned)((nb + kThreads - 1) / kThreads);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
   for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
     const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
     const dim3 g(gx, (unsigned)nf);
     if (img_is_f64)
-      k_dense_sweep<double><<<g, kThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M, r_min,
+      k_dense_sweep<double><<<g, kRowThreads, 0, s>>>((const double*)img + f0 * (int64_t)h * w, h, w, nb, M, r_min,
                                                     r_max, sse + f0 * nr);
     else
-      k_dense_sweep<uint8_t><<<g, kThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
+      k_dense_sweep<uint8_t><<<g, kRowThreads, 0, s>>>((const uint8_t*)img + f0 * (int64_t)h * w, h, w, nb, M,
                                                      r_min, r_max, sse + f0 * nr);
     ADCT_CUDA_TRY(cudaGetLastError());
   }

@@ -179,8 +179,10 @@ CUfunction build(int kind, const QParamsDev& q) {
   const char* expr = kernel_expression(kind);
   CUfunction fn = nullptr;
   bool good = expr != nullptr && nv.add_name(prog, expr) == 0;
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
-  if (good && nv.compile(prog, 3, opts) != 0) {
+  // ADCT_JIT_OPTS: one extra NVRTC option (e.g. -DADCT_QP_FOLD=0) for A/B runs
+  const char* extra = std::getenv("ADCT_JIT_OPTS");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", extra ? extra : ""};
+  if (good && nv.compile(prog, extra ? 4 : 3, opts) != 0) {
     good = false;
     if (std::getenv("ADCT_QUANT_JIT_LOG")) {
       size_t n = 0;

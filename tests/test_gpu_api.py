@@ -334,3 +334,22 @@ def test_config3_full_batch_properties(cuda):
         wr, ws, _ = exact.compress_retain(x[i].cpu().numpy(), 10)
         assert int(sse[i]) == ws and np.array_equal(rec[i].cpu().numpy(), wr)
     assert int(h1.sum()) > 0
+
+
+def test_forward_unscaled_device_tensors(cuda):
+    """Device tensors route by dtype (no value scan, no host sync): uint8 takes
+    the exact integer kernel, other dtypes the dense float64 kernel with K,
+    exact for integer values and returned in the input's kind."""
+    rng = np.random.default_rng(7)
+    ib = rng.integers(-1024, 1025, (6, 8, 8))
+    want = exact.T @ ib @ exact.T.T
+    for dt in (torch.int32, torch.int64, torch.float32, torch.float64):
+        z = codec.forward_2d_unscaled(T, torch.as_tensor(ib, dtype=dt, device=cuda))
+        assert z.is_cuda and np.array_equal(z.cpu().numpy(), want), dt
+        assert (z.dtype == torch.int64) == (not dt.is_floating_point)
+    u8 = rng.integers(0, 256, (3, 8, 8)).astype(np.uint8)
+    z = codec.forward_2d_unscaled(T, torch.as_tensor(u8, device=cuda))
+    assert z.dtype == torch.int64 and np.array_equal(z.cpu().numpy(), exact.T @ u8.astype(np.int64) @ exact.T.T)
+    fb = rng.normal(0, 50, (4, 8, 8))
+    zf = codec.forward_2d_unscaled(T, torch.as_tensor(fb, device=cuda))
+    assert np.abs(zf.cpu().numpy() - exact.T @ fb @ exact.T.T).max() < 1e-9
