@@ -1061,59 +1061,132 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------------------
 // Float64 transforms (real-valued inputs; signature parity with the
-// reference's float API).  Eight threads per 8x8 block, one block row each
-// (a warp holds 4 blocks): a thread loads / stores one contiguous 8-value row
-// (the 8 threads of a block cover the block's 512 coefficient bytes, a warp
-// 2 KB contiguous), runs the 1-D transform on it, and the row <-> column
-// turns go through a padded per-warp shared-memory tile (xpose8).  Register
-// footprint is 8 values per thread instead of a whole block, so nothing
-// spills and 2 CTAs of 256 threads x 8 warps stay resident per SM.
+// reference's float API).  Eight threads per 8x8 block, one block row or
+// column each (a warp holds 4 consecutive blocks).  Every global access goes
+// through a padded per-warp shared-memory tile [4 blocks][8 rows][9]:
+// pixels arrive one image row segment (4 blocks x 8 values, 32 consecutive
+// elements) per warp instruction and coefficients as the warp's 256
+// contiguous doubles, 32 per instruction, so every load and store is
+// coalesced; the 1-D passes read a row or a column of the tile (the 9-value
+// pitch keeps both conflict-free).  8 values per thread in registers.
 // ---------------------------------------------------------------------------
 constexpr int kRowThreads = 256;               // threads per CTA: 32 blocks
 constexpr int kRowBlocks = kRowThreads / 8;    // blocks per CTA
-constexpr int kXposeWarp = 4 * 8 * 9;          // doubles per warp tile (4 blocks x 8 rows, padded to 9)
+constexpr int kXposeWarp = 4 * 8 * 9;          // doubles per warp tile
+
+// zigzag rank -> position u*8+v (ZIGZAG_INDICES, codec.py:24-33)
+__constant__ unsigned char kZigzagPos[64] = {
+    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,  12, 19, 26, 33, 40, 48,
+    41, 34, 27, 20, 13, 6,  7,  14, 21, 28, 35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23,
+    30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+
+// Bit p set for the first r zigzag positions (a uniform loop: the same for
+// every thread, no per-element rank computation).
+__device__ __forceinline__ unsigned long long zz_keep_mask(int r) {
+  unsigned long long m = 0;
+  for (int k = 0; k < r; ++k) m |= 1ull << kZigzagPos[k];
+  return m;
+}
 
 __device__ __forceinline__ double dscale(int u) {
   // d = (1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2, 1/sqrt8, 1/sqrt2, 1/2, 1/sqrt2), kernels.py:149-157
   return (u & 1) ? 0.70710678118654757 : ((u & 2) ? 0.5 : 0.35355339059327379);
 }
 
-// This thread's block and row.  `buf` = the warp's transpose tile.
 struct RowLoc {
-  int64_t blk;  // block index within the frame
+  int64_t blk0;  // first block of this warp (within the frame)
   int64_t frame;
-  int i;        // row of the block this thread owns
-  int g;        // block slot within the warp (0..3)
-  bool active;
-  double* buf;
+  int i;         // row / column of its block this thread owns
+  int g;         // the thread's block within the warp (0..3)
+  int lane;
+  int64_t nblocks;
+  double* buf;   // the warp's tile
 };
 
 __device__ __forceinline__ RowLoc row_locate(int64_t nblocks, double* tiles) {
   RowLoc L;
-  L.blk = (int64_t)blockIdx.x * kRowBlocks + (threadIdx.x >> 3);
+  L.lane = threadIdx.x & 31;
+  L.blk0 = (int64_t)blockIdx.x * kRowBlocks + (threadIdx.x >> 5) * 4;
   L.frame = blockIdx.y;
-  L.i = threadIdx.x & 7;
-  L.g = (threadIdx.x >> 3) & 3;
-  L.active = L.blk < nblocks;
+  L.i = L.lane & 7;
+  L.g = L.lane >> 3;
+  L.nblocks = nblocks;
   L.buf = tiles + (threadIdx.x >> 5) * kXposeWarp;
   return L;
 }
 
-// Row <-> column turn within each block: thread i of block g gives in[v]
-// (its row) and gets out[u] = in[i] of thread u.  The 9-double row pitch
-// keeps both the stores and the strided loads free of bank conflicts.
-__device__ __forceinline__ void xpose8(const RowLoc& L, const double (&in)[8], double (&out)[8]) {
+__device__ __forceinline__ double& tile_at(const RowLoc& L, int g, int row, int col) {
+  return L.buf[(g * 8 + row) * 9 + col];
+}
+__device__ __forceinline__ void tile_get_row(const RowLoc& L, double (&r)[8]) {
 #pragma unroll
-  for (int v = 0; v < 8; ++v) L.buf[(L.g * 8 + L.i) * 9 + v] = in[v];
-  __syncwarp();
+  for (int v = 0; v < 8; ++v) r[v] = tile_at(L, L.g, L.i, v);
+}
+__device__ __forceinline__ void tile_put_row(const RowLoc& L, const double (&r)[8]) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) out[u] = L.buf[(L.g * 8 + u) * 9 + L.i];
+  for (int v = 0; v < 8; ++v) tile_at(L, L.g, L.i, v) = r[v];
+}
+__device__ __forceinline__ void tile_get_col(const RowLoc& L, double (&c)[8]) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) c[u] = tile_at(L, L.g, u, L.i);
+}
+__device__ __forceinline__ void tile_put_col(const RowLoc& L, const double (&c)[8]) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) tile_at(L, L.g, u, L.i) = c[u];
+}
+
+// Image rows of the warp's 4 blocks -> tile (row k of block g at [g][k][*]).
+// Instruction k reads row k of all four blocks: 32 consecutive elements when
+// the blocks share a block row.  Blocks past the end read as 0.
+template <typename InT>
+__device__ __forceinline__ void tile_load_image(const RowLoc& L, const InT* img, int h, int w) {
+  const int64_t blk = L.blk0 + L.g, nbc = w / 8;
+  const bool on = blk < L.nblocks;
+  const int64_t brow = blk / nbc, bcol = blk - brow * nbc;
+  const InT* src = img + L.frame * (int64_t)h * w + brow * 8 * w + bcol * 8 + L.i;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tile_at(L, L.g, k, L.i) = on ? (double)src[(int64_t)k * w] : 0.0;
   __syncwarp();
 }
 
-__device__ __forceinline__ const double* image_row(const double* img, const RowLoc& L, int h, int w, int64_t nbc) {
-  const int64_t brow = L.blk / nbc, bcol = L.blk - brow * nbc;
-  return img + L.frame * (int64_t)h * w + (brow * 8 + L.i) * w + bcol * 8;
+__device__ __forceinline__ void tile_store_image(const RowLoc& L, double* out, int h, int w, int clamp) {
+  __syncwarp();
+  const int64_t blk = L.blk0 + L.g, nbc = w / 8;
+  if (blk >= L.nblocks) return;
+  const int64_t brow = blk / nbc, bcol = blk - brow * nbc;
+  double* dst = out + L.frame * (int64_t)h * w + brow * 8 * w + bcol * 8 + L.i;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double v = tile_at(L, L.g, k, L.i);
+    dst[(int64_t)k * w] = clamp ? fmin(fmax(v, 0.0), 255.0) : v;
+  }
+}
+
+// The warp's 4 x 64 contiguous coefficients <-> tile, 32 per instruction.
+// Element e = 32 k + lane is block e / 64, row (e % 64) / 8, column e % 8.
+__device__ __forceinline__ void tile_store_coef(const RowLoc& L, double* coef) {
+  __syncwarp();
+  double* dst = coef + (L.frame * L.nblocks + L.blk0) * 64;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = 32 * k + L.lane, g = e >> 6;
+    if (L.blk0 + g < L.nblocks) dst[e] = tile_at(L, g, (e >> 3) & 7, e & 7);
+  }
+}
+
+// SCALE: multiply by d_u d_v (the proposed transform's D); r: zigzag mask.
+template <bool SCALE>
+__device__ __forceinline__ void tile_load_coef(const RowLoc& L, const double* coef, int r) {
+  const double* src = coef + (L.frame * L.nblocks + L.blk0) * 64;
+  const unsigned long long keep = zz_keep_mask(r);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = 32 * k + L.lane, g = e >> 6, u = (e >> 3) & 7, v = e & 7;
+    double val = 0.0;
+    if (L.blk0 + g < L.nblocks && ((keep >> (e & 63)) & 1)) val = SCALE ? src[e] * (dscale(u) * dscale(v)) : src[e];
+    tile_at(L, g, u, v) = val;
+  }
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -1121,25 +1194,20 @@ __global__ void __launch_bounds__(kRowThreads)
                   double* __restrict__ coef) {
   __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
   const RowLoc L = row_locate(nblocks, tiles);
-  double x[8], t[8], c[8], Z[8];
-  if (L.active) {
-    const double* src = image_row(img, L, h, w, w / 8);
+  double a[8], b[8];
+  tile_load_image(L, img, h, w);
+  tile_get_col(L, a);   // column i of X
+  fwd8(a, b);           // (T X)[u][i]
+  __syncwarp();
+  tile_put_col(L, b);
+  __syncwarp();
+  tile_get_row(L, a);   // row i of T X
+  fwd8(a, b);           // Z[i][v] = (T X T^T)[i][v]
 #pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = src[j];
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = 0.0;
-  }
-  fwd8(x, t);        // row i: t[i][v] = (T x_i)[v]
-  xpose8(L, t, c);   // column i: c[u'] = t[u'][i]
-  fwd8(c, Z);        // Z[u][i]
-#pragma unroll
-  for (int u = 0; u < 8; ++u) Z[u] *= dscale(u) * dscale(L.i);
-  xpose8(L, Z, t);   // row i of the scaled coefficients
-  if (!L.active) return;
-  double* dst = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
-#pragma unroll
-  for (int v = 0; v < 8; ++v) dst[v] = t[v];
+  for (int v = 0; v < 8; ++v) b[v] *= dscale(L.i) * dscale(v);
+  __syncwarp();
+  tile_put_row(L, b);
+  tile_store_coef(L, coef);
 }
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -1147,23 +1215,18 @@ __global__ void __launch_bounds__(kRowThreads)
                   int clamp, double* __restrict__ out) {
   __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
   const RowLoc L = row_locate(nblocks, tiles);
-  double W[8], c[8], col[8], x[8];
-  if (L.active) {
-    const double* src = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
-#pragma unroll
-    for (int v = 0; v < 8; ++v) W[v] = (zz_rank(L.i, v) < r) ? src[v] * (dscale(L.i) * dscale(v)) : 0.0;
-  } else {
-#pragma unroll
-    for (int v = 0; v < 8; ++v) W[v] = 0.0;
-  }
-  inv8(W, c);          // row u = i: c[u][j] = (T^T W_u)[j]
-  xpose8(L, c, col);   // column j = i: col[u] = c[u][i]
-  inv8(col, x);        // x[i'][j] for i' = 0..7
-  xpose8(L, x, c);     // row i of the reconstruction
-  if (!L.active) return;
-  double* dst = const_cast<double*>(image_row(out, L, h, w, w / 8));
-#pragma unroll
-  for (int j = 0; j < 8; ++j) dst[j] = clamp ? fmin(fmax(c[j], 0.0), 255.0) : c[j];
+  double a[8], b[8];
+  tile_load_coef<true>(L, coef, r);
+  tile_get_row(L, a);   // row u = i of W
+  inv8(a, b);           // (W T)[i][j]
+  __syncwarp();
+  tile_put_row(L, b);
+  __syncwarp();
+  tile_get_col(L, a);   // column j = i of W T
+  inv8(a, b);           // x[i'][j] = (T^T W T)[i'][j]
+  __syncwarp();
+  tile_put_col(L, b);
+  tile_store_image(L, out, h, w, clamp);
 }
 
 // ---------------------------------------------------------------------------
@@ -1237,41 +1300,23 @@ __device__ __forceinline__ void dense8t(const DenseMat& M, const double (&y)[8],
 }
 
 template <typename InT>
-__device__ __forceinline__ void load_row_f64(const InT* img, const RowLoc& L, int h, int w, double (&x)[8]) {
-  if (!L.active) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = 0.0;
-    return;
-  }
-  const int64_t nbc = w / 8, brow = L.blk / nbc, bcol = L.blk - brow * nbc;
-  const InT* src = img + L.frame * (int64_t)h * w + (brow * 8 + L.i) * w + bcol * 8;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) x[j] = (double)src[j];
-}
-
-// Column i of Y = C X C^T for this thread's block (Yc[u] = Y[u][i]).
-__device__ __forceinline__ void dense_fwd_cols(const DenseMat& M, const RowLoc& L, const double (&x)[8],
-                                               double (&Yc)[8]) {
-  double t[8], c[8];
-  dense8(M, x, t);   // row i: t[i][v] = (C x_i)[v]
-  xpose8(L, t, c);   // column i: c[i'] = t[i'][i]
-  dense8(M, c, Yc);  // Y[u][i]
-}
-
-template <typename InT>
 __global__ void __launch_bounds__(kRowThreads)
     k_dense_forward(const InT* __restrict__ img, int h, int w, int64_t nblocks, const DenseMat M,
                     double* __restrict__ coef) {
   __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
   const RowLoc L = row_locate(nblocks, tiles);
-  double x[8], Yc[8], Yr[8];
-  load_row_f64(img, L, h, w, x);
-  dense_fwd_cols(M, L, x, Yc);
-  xpose8(L, Yc, Yr);  // row i of Y
-  if (!L.active) return;
-  double* dst = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
-#pragma unroll
-  for (int v = 0; v < 8; ++v) dst[v] = Yr[v];
+  double a[8], b[8];
+  tile_load_image(L, img, h, w);
+  tile_get_col(L, a);   // column i of X
+  dense8(M, a, b);      // (C X)[u][i]
+  __syncwarp();
+  tile_put_col(L, b);
+  __syncwarp();
+  tile_get_row(L, a);   // row i of C X
+  dense8(M, a, b);      // Y[i][v] = (C X C^T)[i][v]
+  __syncwarp();
+  tile_put_row(L, b);
+  tile_store_coef(L, coef);
 }
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -1279,34 +1324,25 @@ __global__ void __launch_bounds__(kRowThreads)
                     const DenseMat M, double* __restrict__ out) {
   __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
   const RowLoc L = row_locate(nblocks, tiles);
-  double Y[8], c[8], col[8], x[8];
-  if (L.active) {
-    const double* src = coef + (L.frame * nblocks + L.blk) * 64 + L.i * 8;
-#pragma unroll
-    for (int v = 0; v < 8; ++v) Y[v] = (zz_rank(L.i, v) < r) ? src[v] : 0.0;
-  } else {
-#pragma unroll
-    for (int v = 0; v < 8; ++v) Y[v] = 0.0;
-  }
-  dense8t(M, Y, c);     // row u = i: c[u][j] = (C^T Y_u)[j]
-  xpose8(L, c, col);    // column j = i
-  dense8t(M, col, x);   // x[i'][j]
-  xpose8(L, x, c);      // row i
-  if (!L.active) return;
-  double* dst = const_cast<double*>(image_row(out, L, h, w, w / 8));
-#pragma unroll
-  for (int j = 0; j < 8; ++j) dst[j] = clamp ? fmin(fmax(c[j], 0.0), 255.0) : c[j];
+  double a[8], b[8];
+  tile_load_coef<false>(L, coef, r);
+  tile_get_row(L, a);   // row u = i of Y
+  dense8t(M, a, b);     // (Y C)[i][j]
+  __syncwarp();
+  tile_put_row(L, b);
+  __syncwarp();
+  tile_get_col(L, a);   // column j = i of Y C
+  dense8t(M, a, b);     // x[i'][j] = (C^T Y C)[i'][j]
+  __syncwarp();
+  tile_put_col(L, b);
+  tile_store_image(L, out, h, w, clamp);
 }
 
 // r-sweep: the block's Y waits in shared memory (read once per r at the
 // zigzag position, a broadcast within each block's 8 threads); each thread
 // updates its reconstruction row (8 FMAs per r) and adds its clamped squared
 // errors; per r a warp reduction into a per-warp shared partial, one atomic
-// per (CTA, r) at the end.
-__constant__ unsigned char kZigzagPos[64] = {
-    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,  12, 19, 26, 33, 40, 48,
-    41, 34, 27, 20, 13, 6,  7,  14, 21, 28, 35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23,
-    30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+// per (CTA, r) at the end.  kZigzagPos (zigzag rank -> u*8+v) is above.
 
 template <typename InT>
 __global__ void __launch_bounds__(kRowThreads)
@@ -1317,27 +1353,35 @@ __global__ void __launch_bounds__(kRowThreads)
   __shared__ double cs[64];                          // C
   __shared__ double part[64][kRowThreads / 32];      // [r - r_min][warp]
   const RowLoc L = row_locate(nblocks, tiles);
+  const bool active = L.blk0 + L.g < nblocks;
   const int nr = r_max - r_min + 1;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x < 64) cs[threadIdx.x] = M.c[threadIdx.x];
-  double x[8], Yc[8], V[8];
-  load_row_f64(img, L, h, w, x);
-  dense_fwd_cols(M, L, x, Yc);
+  double x[8], a[8], b[8], V[8];
+  tile_load_image(L, img, h, w);
+  tile_get_row(L, x);   // row i of X, kept for the SSE
+  tile_get_col(L, a);
+  dense8(M, a, b);      // (C X)[u][i]
+  __syncwarp();
+  tile_put_col(L, b);
+  __syncwarp();
+  tile_get_row(L, a);
+  dense8(M, a, b);      // Y[i][v]
   double* yb = ys + (threadIdx.x >> 3) * 64;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) yb[u * 8 + L.i] = Yc[u];
+  for (int v = 0; v < 8; ++v) yb[L.i * 8 + v] = b[v];
 #pragma unroll
   for (int j = 0; j < 8; ++j) V[j] = 0.0;
   __syncthreads();  // cs, ys
 #pragma unroll 1
   for (int k = 0; k < r_max; ++k) {
     const int pos = kZigzagPos[k], u = pos >> 3, v = pos & 7;
-    const double a = yb[pos] * cs[u * 8 + L.i];
+    const double c = yb[pos] * cs[u * 8 + L.i];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) V[j] = fma(a, cs[v * 8 + j], V[j]);
+    for (int j = 0; j < 8; ++j) V[j] = fma(c, cs[v * 8 + j], V[j]);
     if (k + 1 < r_min) continue;
     double acc = 0.0;
-    if (L.active) {
+    if (active) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const double d = x[j] - fmin(fmax(V[j], 0.0), 255.0);
@@ -1346,7 +1390,7 @@ __global__ void __launch_bounds__(kRowThreads)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) part[k + 1 - r_min][warp] = acc;
+    if (L.lane == 0) part[k + 1 - r_min][warp] = acc;
   }
   __syncthreads();
   if (threadIdx.x < nr) {
