@@ -233,6 +233,10 @@ int adct_sweep_dense(const void* img, int32_t img_is_f64, int64_t n, int32_t h, 
  * img/out: device float64 [n][h][w]; coef: device float64 [n][h*w/64][8][8]. */
 int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w,
                      double* coef, void* stream);
+/* Same for uint8 images (the reference converts them to float64 first,
+ * codec.py:127; here the kernel reads the bytes: 1 B per pixel in). */
+int adct_forward_f64_u8(const uint8_t* img, int64_t n, int32_t h, int32_t w,
+                        double* coef, void* stream);
 int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w,
                      int32_t r, int32_t clamp, double* out, void* stream);
 

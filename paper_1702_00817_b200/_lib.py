@@ -101,6 +101,7 @@ PROTOTYPES = {
         [c_void_p, c_int32, c_int64, c_int32, c_int32, POINTER(c_double), c_int32, c_int32, c_void_p, c_void_p],
     ),
     "adct_forward_f64": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    "adct_forward_f64_u8": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "adct_inverse_f64": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "adct_sse_u8": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
     "adct_synth_blobs": (c_int, [c_void_p, c_int64, c_int32, c_int32, c_int64, c_void_p, c_int32, c_void_p, c_void_p]),

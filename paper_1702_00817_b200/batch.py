@@ -322,9 +322,10 @@ def forward_f64(images: torch.Tensor) -> torch.Tensor:
     n, h, w = images.shape
     if h % 8 or w % 8:
         raise BadDimensions(f"image dimensions must be divisible by 8, got {(h, w)}")
-    x = images.to(dtype=torch.float64).contiguous()
+    u8 = images.dtype == torch.uint8  # read as bytes by the kernel, no float64 copy
+    x = images.contiguous() if u8 else images.to(dtype=torch.float64).contiguous()
     coef = torch.empty((n, (h // 8) * (w // 8), 8, 8), dtype=torch.float64, device=x.device)
-    _lib.call("adct_forward_f64", _ptr(x), n, h, w, _ptr(coef), _stream())
+    _lib.call("adct_forward_f64_u8" if u8 else "adct_forward_f64", _ptr(x), n, h, w, _ptr(coef), _stream())
     return coef
 
 

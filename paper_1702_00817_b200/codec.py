@@ -92,6 +92,14 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _image_dtype(a) -> torch.dtype:
+    """uint8 images travel and are read as bytes (1/8 of the float64 copy the
+    reference makes, codec.py:127); anything else as float64."""
+    if isinstance(a, torch.Tensor):
+        return torch.uint8 if a.dtype == torch.uint8 else torch.float64
+    return torch.uint8 if np.asarray(a).dtype == np.uint8 else torch.float64
+
+
 def _to_dev(a, dtype=None) -> tuple[torch.Tensor, bool]:
     """(tensor on device, was_numpy)."""
     if isinstance(a, torch.Tensor):
@@ -157,7 +165,7 @@ def _blocks_as_images(block) -> tuple[object, tuple]:
 
 def forward_2d(t, block):
     """C B C^T (codec.py:68-71), float64, over (..., 8, 8)."""
-    x, was_np = _to_dev(block, torch.float64)
+    x, was_np = _to_dev(block, _image_dtype(block))
     xs, lead = _blocks_as_images(x)
     y = batch.forward_f64(xs) if is_proposed(t) else batch.forward_dense(xs, _matrix(t))
     return _back(y.reshape(*lead, 8, 8) if lead else y.reshape(8, 8), was_np)
@@ -200,7 +208,7 @@ def coefficient_blocks(t, image):
     shape = tuple(image.shape)
     if len(shape) != 2 or shape[0] % 8 or shape[1] % 8:
         raise BadDimensions(f"image dimensions must be divisible by 8, got {shape}")
-    x, was_np = _to_dev(image, torch.float64)
+    x, was_np = _to_dev(image, _image_dtype(image))
     c = batch.forward_f64(x.unsqueeze(0)) if is_proposed(t) else batch.forward_dense(x.unsqueeze(0), _matrix(t))
     return _back(c[0], was_np)
 
@@ -226,7 +234,7 @@ def compress_image(t, image, r: int):
     if len(shape) != 2 or shape[0] % 8 or shape[1] % 8:
         raise BadDimensions(f"image dimensions must be divisible by 8, got {shape}")
     m = None if is_proposed(t) else _matrix(t)
-    x, was_np = _to_dev(image, torch.float64)
+    x, was_np = _to_dev(image, _image_dtype(image))
     if m is None:
         c = batch.forward_f64(x.unsqueeze(0))
         out = batch.inverse_f64(c, shape[0], shape[1], r=int(r), clamp=True)[0]

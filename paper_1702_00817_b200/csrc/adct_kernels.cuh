@@ -1189,8 +1189,9 @@ __device__ __forceinline__ void tile_load_coef(const RowLoc& L, const double* co
   __syncwarp();
 }
 
+template <typename InT>
 __global__ void __launch_bounds__(kRowThreads)
-    k_forward_f64(const double* __restrict__ img, int h, int w, int64_t nblocks,
+    k_forward_f64(const InT* __restrict__ img, int h, int w, int64_t nblocks,
                   double* __restrict__ coef) {
   __shared__ double tiles[kRowThreads / 32 * kXposeWarp];
   const RowLoc L = row_locate(nblocks, tiles);

@@ -437,6 +437,32 @@ inline int32_t round_half_away_pos(double x) { return (int32_t)std::floor(x + 0.
 }  // namespace
 
 // ===========================================================================
+static int f64_geometry(int64_t n, int32_t h, int32_t w, int64_t& nblocks) {
+  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
+  if (h < 0 || w < 0 || (h % 8) || (w % 8)) return ADCT_ERR_BAD_DIMENSIONS;
+  nblocks = (int64_t)(h / 8) * (w / 8);
+  if (nblocks > (int64_t)kThreads * 0x7FFFFFFF) return ADCT_ERR_INVALID_ARGUMENT;
+  return ADCT_OK;
+}
+
+template <typename InT>
+static int forward_f64_impl(const InT* img, int64_t n, int32_t h, int32_t w, double* coef, void* stream) {
+  int64_t nb;
+  int rc = f64_geometry(n, h, w, nb);
+  if (rc != ADCT_OK) return rc;
+  if (n == 0 || nb == 0) return ADCT_OK;
+  if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
+  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
+    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
+    k_forward_f64<InT><<<dim3(gx, (unsigned)nf), kRowThreads, 0, s>>>(img + f0 * (int64_t)h * w, h, w, nb,
+                                                                     coef + f0 * nb * 64);
+    ADCT_CUDA_TRY(cudaGetLastError());
+  }
+  return ADCT_OK;
+}
+
 extern "C" {
 
 int adct_version(void) { return 1 * 10000 + 0 * 100 + 0; }
@@ -802,30 +828,13 @@ int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, i
 }
 
 // --- float64 -----------------------------------------------------------------
-static int f64_geometry(int64_t n, int32_t h, int32_t w, int64_t& nblocks) {
-  if (n < 0) return ADCT_ERR_INVALID_ARGUMENT;
-  if (h < 0 || w < 0 || (h % 8) || (w % 8)) return ADCT_ERR_BAD_DIMENSIONS;
-  nblocks = (int64_t)(h / 8) * (w / 8);
-  if (nblocks > (int64_t)kThreads * 0x7FFFFFFF) return ADCT_ERR_INVALID_ARGUMENT;
-  return ADCT_OK;
+
+int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w, double* coef, void* stream) {
+  return forward_f64_impl(img, n, h, w, coef, stream);
 }
 
-int adct_forward_f64(const double* img, int64_t n, int32_t h, int32_t w, double* coef,
-                     void* stream) {
-  int64_t nb;
-  int rc = f64_geometry(n, h, w, nb);
-  if (rc != ADCT_OK) return rc;
-  if (n == 0 || nb == 0) return ADCT_OK;
-  if (img == nullptr || coef == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
-  cudaStream_t s = as_stream(stream);
-  const unsigned gx = (unsigned)((nb + kRowBlocks - 1) / kRowBlocks);
-  for (int64_t f0 = 0; f0 < n; f0 += kMaxGridY) {
-    const int64_t nf = (n - f0) < kMaxGridY ? (n - f0) : kMaxGridY;
-    k_forward_f64<<<dim3(gx, (unsigned)nf), kRowThreads, 0, s>>>(img + f0 * (int64_t)h * w, h, w, nb,
-                                                               coef + f0 * nb * 64);
-    ADCT_CUDA_TRY(cudaGetLastError());
-  }
-  return ADCT_OK;
+int adct_forward_f64_u8(const uint8_t* img, int64_t n, int32_t h, int32_t w, double* coef, void* stream) {
+  return forward_f64_impl(img, n, h, w, coef, stream);
 }
 
 int adct_inverse_f64(const double* coef, int64_t n, int32_t h, int32_t w, int32_t r, int32_t clamp,
