@@ -716,7 +716,9 @@ def gpu_arm(args) -> None:
     secondary = {}
     if args.config == 3 and not args.no_secondary:
         # the quantised kernels measured in the same run (same box, same clock record)
-        for c, steps in ((4, max(3, min(args.steps, 20))), (2, max(3, min(args.steps, 50)))):
+        # (config 2's step is ~0.4 ms: 10x the steps keep the timed region long
+        # enough for the 50 ms nvidia-smi clock sampler to see it)
+        for c, steps in ((4, max(3, min(args.steps, 20))), (2, max(3, min(10 * args.steps, 1000)))):
             s = measure(c, args, rank, world, local, dev, steps, max(args.warmup, 4), with_e2e=False, with_cpu=False)
             secondary[f"config{c}"] = {
                 "value": s["value"], "unit": UNIT, "steps": steps, "ms_per_step": s["elapsed_ms"] / steps,
