@@ -109,3 +109,24 @@ def test_extreme_geometries(cuda, h, w):
         assert int(sse[0]) == int((d * d).sum())
         dq = recq.to(torch.int64) - x.to(torch.int64)
         assert int(sseq[0]) == int((dq * dq).sum())
+
+
+@pytest.mark.parametrize("h,w", [(8, 65536), (65536, 16), (8, 16), (16384, 16384)])
+def test_extreme_geometries_float_inverse(cuda, h, w):
+    """The same extremes through k_quant_fi (q = 10: 128-unit tiles, the
+    park in shared memory): exact where cheap, sampled bands otherwise."""
+    g = torch.Generator().manual_seed(3 * h + w)
+    x = torch.randint(0, 256, (1, h, w), dtype=torch.uint8, generator=g).to(cuda)
+    qt = quant.quant_table(10)
+    recq, sseq = batch.compress_quant(x, qt)
+    torch.cuda.synchronize()
+    if h * w <= (1 << 20):
+        wq, wqs = exact.compress_quant(x.cpu().numpy(), quant.qtab_qprime(qt))
+        assert np.array_equal(recq.cpu().numpy(), wq) and np.array_equal(sseq.cpu().numpy(), wqs)
+    else:
+        for r0 in (0, h // 2, h - 64):
+            band = x[:, r0:r0 + 64].contiguous().cpu().numpy()
+            wq, _ = exact.compress_quant(band, quant.qtab_qprime(qt))
+            assert np.array_equal(recq[:, r0:r0 + 64].cpu().numpy(), wq), r0
+        dq = recq.to(torch.int64) - x.to(torch.int64)
+        assert int(sseq[0]) == int((dq * dq).sum())

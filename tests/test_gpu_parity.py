@@ -131,15 +131,19 @@ def test_ragged_width_retain_and_quant(cuda):
     assert np.array_equal(recq.cpu().numpy(), wq) and np.array_equal(sseq.cpu().numpy(), wqs)
 
 
-def test_planes_quant_one_launch(cuda):
+@pytest.mark.parametrize("q", [10, 75])
+def test_planes_quant_one_launch(cuda, q):
+    """Y + Cb + Cr in one launch: q = 75 on the packed kernel, q = 10 on the
+    float-pair-inverse kernel (tiles of 128 units; the planes' unit counts are
+    not multiples of the tile)."""
     g = torch.Generator().manual_seed(5)
     y = torch.randint(0, 256, (2, 64, 96), dtype=torch.uint8, generator=g)
     cb = torch.randint(0, 256, (2, 32, 48), dtype=torch.uint8, generator=g)
     cr = torch.randint(0, 256, (2, 32, 48), dtype=torch.uint8, generator=g)
-    qt = quant.quant_table(75)
+    qt = quant.quant_table(q)
     recs, sse = batch.compress_quant_planes([y.to(cuda), cb.to(cuda), cr.to(cuda)], qt)
     torch.cuda.synchronize()
-    qp = exact.qprime(quant.q50_luma(), 75)
+    qp = exact.qprime(quant.q50_luma(), q)
     for k, p in enumerate((y, cb, cr)):
         wr, ws = exact.compress_quant(p.numpy(), qp)
         assert np.array_equal(recs[k].cpu().numpy(), wr)
