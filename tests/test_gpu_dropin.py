@@ -134,3 +134,53 @@ def test_reference_errors_and_functions_through_dispatch(adct_pkg, dispatch):
         adct.codec.coefficient_blocks(t, np.zeros((12, 16)))
     with pytest.raises(adct.errors.DimensionMismatch):
         adct.metrics.mse(np.zeros((8, 8)), np.zeros((8, 16)))
+
+
+def _read_csv(path):
+    import csv
+
+    with open(path) as fp:
+        return list(csv.reader(fp))
+
+
+def _assert_csv_close(a, b):
+    """Same rows and text cells; numeric cells (printed to 6 significant
+    digits by the reference) equal to that precision."""
+    assert len(a) == len(b) and a[0] == b[0]
+    for ra, rb in zip(a[1:], b[1:]):
+        assert len(ra) == len(rb)
+        for x, y in zip(ra, rb):
+            try:
+                fx, fy = float(x), float(y)
+            except ValueError:
+                assert x == y
+                continue
+            assert fx == pytest.approx(fy, rel=2e-6, abs=1e-12) or (np.isnan(fx) and np.isnan(fy)), (ra, rb)
+
+
+@pytest.mark.parametrize("corpus", ["synthetic", "pgm"])
+def test_reference_sweep_command_with_driver_dispatch(adct_pkg, dispatch, tmp_path, corpus):
+    """enable(drivers=True): the unmodified `adct sweep` command (cli.main ->
+    cmd_sweep -> run_sweep -> _write_sweep_outputs) runs the batched GPU sweep
+    and writes the reference's own records.csv / summary.csv / metadata."""
+    adct = adct_pkg
+    names = ["dct", "proposed", sorted(adct.kernels.default_registry().names())[0]]
+    args = ["sweep", "--transforms", ",".join(names), "--r-min", "1", "--r-max", "45"]
+    if corpus == "pgm":  # uint8 images: the exact integer sweep for "proposed"
+        d = tmp_path / "corpus"
+        d.mkdir()
+        for k, im in enumerate(synth.images_np(range(3), 64, 96, 16, 8.0, 64.0)):
+            pgm.write_pgm_u8(im, d / f"im{k}.pgm")
+        args += ["--corpus", str(d)]
+    else:  # the reference's float synthesizer: dense float64 sweeps
+        args += ["--n-images", "3", "--seed", "5"]
+    orig = adct.cli.run_sweep
+    assert adct.cli.main(args + ["--out", str(tmp_path / "ref")]) == 0
+    dispatch["enable"](drivers=True)
+    assert adct.cli.run_sweep is not orig
+    assert adct.cli.main(args + ["--out", str(tmp_path / "gpu")]) == 0
+    for f in ("records.csv", "summary.csv"):
+        _assert_csv_close(_read_csv(tmp_path / "gpu" / f), _read_csv(tmp_path / "ref" / f))
+    assert (tmp_path / "gpu" / "run_metadata.json").read_text() == (tmp_path / "ref" / "run_metadata.json").read_text()
+    dispatch["disable"]()
+    assert adct.cli.run_sweep is orig
