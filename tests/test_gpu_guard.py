@@ -130,3 +130,29 @@ def test_extreme_geometries_float_inverse(cuda, h, w):
             assert np.array_equal(recq[:, r0:r0 + 64].cpu().numpy(), wq), r0
         dq = recq.to(torch.int64) - x.to(torch.int64)
         assert int(sseq[0]) == int((dq * dq).sum())
+
+
+def test_more_frames_than_one_grid_row(cuda):
+    """More than 65,535 frames: the launches are chunked along grid.y
+    (frame_base), the persistent quant kernel walks them in one grid.  Every
+    kernel family, exact against the oracle on every frame."""
+    n = 65_535 + 70
+    g = torch.Generator().manual_seed(65)
+    x = torch.randint(0, 256, (n, 8, 16), dtype=torch.uint8, generator=g)
+    xd, xh = x.to(cuda), x.numpy()
+    rec, sse, _ = batch.compress_retain(xd, 10)
+    wr, ws, _ = exact.compress_retain(xh, 10)
+    assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws)
+    for q in (75, 10):  # k_quant_p (persistent), k_quant_fi (chunked)
+        qt = quant.quant_table(q)
+        recq, sseq = batch.compress_quant(xd, qt)
+        wq, wqs = exact.compress_quant(xh, quant.qtab_qprime(qt))
+        assert np.array_equal(recq.cpu().numpy(), wq), q
+        assert np.array_equal(sseq.cpu().numpy(), wqs), q
+    z = batch.forward_int(xd)
+    assert np.array_equal(z.cpu().numpy().astype(np.int64), exact.forward_unscaled(xh))
+    s = batch.sweep_retain_sse(xd, 1, 12)
+    assert np.array_equal(s.cpu().numpy(), exact.sweep_sse(xh, 1, 12))
+    c = batch.forward_f64(xd)
+    back = batch.inverse_f64(c, 8, 16, r=64)
+    assert float((back - xd.to(torch.float64)).abs().max()) < 1e-9
