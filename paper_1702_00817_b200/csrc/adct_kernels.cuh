@@ -499,8 +499,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 // on, the two blocks travel as fp32 pairs (A, B) in 64-bit register pairs, so
 // every step of the inverse is one FP32x2 instruction for both blocks on the
 // FMA pipe (the packed integer kernels keep the ALU pipe the busier one).
-// Exact: every value is a multiple of 1/64 below 2^17 in magnitude (24-bit
-// significand), so no add or fused multiply-add ever rounds.
+// Exact: every value is a multiple of 1/64 below 2^18 in magnitude (the host
+// checks the table's bound, fi_exact in capi.cu), i.e. fits the 24-bit
+// significand, so no add or fused multiply-add ever rounds.
 //   * dequantisation folds into the column inverse: each butterfly add
 //     X_a +- X_b becomes FFMA2(q_b, +-k_b, X_a) with k = Q' E / 64 (the
 //     column's DC term is one FMUL2/FFMA2), so the inverse yields x_hat - 128
