@@ -844,6 +844,21 @@ __global__ void __launch_bounds__(kSweepThreads)
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) U[i][j] = kDcRound;  // T^T (kDcRound e0 e0^T) T = kDcRound everywhere
+  // Rounded SSE without the output byte order: the original pixels are
+  // regrouped once per unit into the order of pack_row's first PRMT level
+  // (a_j b_j a_j+1 b_j+1) and flipped by 0x80 like the packed pixels, so
+  // per r a row costs one PRMT level and a signed |a - b| per byte (the 0x80
+  // flip is x - 128 read as a signed byte): no second PRMT level, no XOR.
+  // Unpaired units: B's inputs are 0, so its lanes reconstruct to 0 and its
+  // flipped bytes cancel against the flipped zero bytes of the original.
+  if (!FSSE) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = w[i];
+      w[i] = make_uint4(__byte_perm(v.x, v.z, 0x5140) ^ 0x80808080u, __byte_perm(v.x, v.z, 0x7362) ^ 0x80808080u,
+                        __byte_perm(v.y, v.w, 0x5140) ^ 0x80808080u, __byte_perm(v.y, v.w, 0x7362) ^ 0x80808080u);
+    }
+  }
   const int nr = r_max - r_min + 1;
   u64* out = sse + L.frame * nr;
 #pragma unroll 1
@@ -868,6 +883,19 @@ __global__ void __launch_bounds__(kSweepThreads)
       if (active) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
+          if (!FSSE) {
+            const u32 q[4] = {__byte_perm(clamp_shift<true>(U[i][0]), clamp_shift<true>(U[i][1]), 0x7531),
+                              __byte_perm(clamp_shift<true>(U[i][2]), clamp_shift<true>(U[i][3]), 0x7531),
+                              __byte_perm(clamp_shift<true>(U[i][4]), clamp_shift<true>(U[i][5]), 0x7531),
+                              __byte_perm(clamp_shift<true>(U[i][6]), clamp_shift<true>(U[i][7]), 0x7531)};
+            const u32 ow[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const u32 d = __vabsdiffs4(q[k], ow[k]);
+              acc = __dp4a(d, d, acc);
+            }
+            continue;
+          }
           uint4 o;
           pack_row(U[i], o);
           acc = sse4(w[i].x, o.x, acc);
