@@ -196,7 +196,8 @@ int adct_compress_retain_planes(const adct_plane_t* planes, int32_t n_planes,
  * K7 — retain-r sweep: one read of each image, SSE for every r in
  * [r_min, r_max].  Replaces the per-r loop of cli.run_sweep
  * (cli.py:101-113: reconstruct_image + mse per r).
- * sse:           device uint64 [n][r_max - r_min + 1], rounded reconstructions
+ * sse:           device uint64 [n][r_max - r_min + 1], rounded reconstructions;
+ *                nullable when sse_unrounded is given (then only that is computed)
  * sse_unrounded: device uint64 [n][r_max - r_min + 1], nullable; 4096 x the
  *                reference's own unrounded clamped SSE (exact). */
 int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w,

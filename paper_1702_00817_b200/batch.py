@@ -414,14 +414,16 @@ def sweep_dense_sse(images: torch.Tensor, C, r_min: int, r_max: int) -> torch.Te
 
 
 @_device_guard
-def sweep_retain_sse_unrounded(images: torch.Tensor, r_min: int = 1, r_max: int = 45):
-    """(rounded SSE, 4096 x unrounded SSE), both int64[N, r] — exact."""
+def sweep_retain_sse_unrounded(images: torch.Tensor, r_min: int = 1, r_max: int = 45, *, rounded: bool = True):
+    """(rounded SSE, 4096 x unrounded SSE), both int64[N, r] — exact.
+    rounded=False skips the rounded SSE (returned as None), which is all the
+    reference's own convention (run_sweep) needs."""
     if not (1 <= r_min <= r_max <= 64):
         raise InvalidRetention(f"retention range must satisfy 1 <= r_min <= r_max <= 64, got {r_min}..{r_max}")
     images = _as_batch(images)
     n, h, w = images.shape
-    sse = torch.empty((n, r_max - r_min + 1), dtype=torch.int64, device=images.device)
-    ssef = torch.empty_like(sse)
+    ssef = torch.empty((n, r_max - r_min + 1), dtype=torch.int64, device=images.device)
+    sse = torch.empty_like(ssef) if rounded else None
     _lib.call("adct_sweep_retain_sse", _ptr(images), n, h, w, _img_stride(images), r_min, r_max, _ptr(sse),
               _ptr(ssef), _stream())
     return sse, ssef

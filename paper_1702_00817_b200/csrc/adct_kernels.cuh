@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(kSweepThreads)
     }
   }
   const int nr = r_max - r_min + 1;
-  u64* out = sse + L.frame * nr;
+  u64* out = sse != nullptr ? sse + L.frame * nr : nullptr;
 #pragma unroll 1
   for (int r = 1; r <= r_max; ++r) {
     const int p = c_sweep.zz[r - 1];
@@ -896,13 +896,15 @@ __global__ void __launch_bounds__(kSweepThreads)
             }
             continue;
           }
-          uint4 o;
-          pack_row(U[i], o);
-          acc = sse4(w[i].x, o.x, acc);
-          acc = sse4(w[i].y, o.y, acc);
-          if (PAIR) {
-            acc = sse4(w[i].z, o.z, acc);
-            acc = sse4(w[i].w, o.w, acc);
+          if (sse != nullptr) {  // (FSSE callers may want only the unrounded SSE)
+            uint4 o;
+            pack_row(U[i], o);
+            acc = sse4(w[i].x, o.x, acc);
+            acc = sse4(w[i].y, o.y, acc);
+            if (PAIR) {
+              acc = sse4(w[i].z, o.z, acc);
+              acc = sse4(w[i].w, o.w, acc);
+            }
           }
           if (FSSE) {
             // the reference's unrounded convention, row by row from the input
@@ -924,7 +926,7 @@ __global__ void __launch_bounds__(kSweepThreads)
           }
         }
       }
-      block_add_u32(acc, out + (r - r_min));
+      if (sse != nullptr) block_add_u32(acc, out + (r - r_min));
       if (FSSE) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) accf += __shfl_xor_sync(0xffffffffu, accf, o);

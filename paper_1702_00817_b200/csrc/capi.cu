@@ -800,10 +800,12 @@ int adct_sweep_retain_sse(const uint8_t* img, int64_t n, int32_t h, int32_t w, i
   PlaneSetHost ps;
   int rc = build_planes(&pl, 1, n, ps);
   if (rc != ADCT_OK) return rc;
-  if (sse == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  // at least one output; the rounded one may be skipped when the unrounded is
+  // wanted (incremental kernel only)
+  if (sse == nullptr && (sse_unrounded == nullptr || sweep_kernel_choice() != 1)) return ADCT_ERR_INVALID_ARGUMENT;
   cudaStream_t s = as_stream(stream);
   const size_t nsse = (size_t)n * (size_t)(r_max - r_min + 1);
-  if (nsse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
+  if (nsse && sse) ADCT_CUDA_TRY(cudaMemsetAsync(sse, 0, nsse * sizeof(uint64_t), s));
   if (nsse && sse_unrounded) ADCT_CUDA_TRY(cudaMemsetAsync(sse_unrounded, 0, nsse * sizeof(uint64_t), s));
   u64* d_sse = reinterpret_cast<u64*>(sse);
   u64* d_ssef = reinterpret_cast<u64*>(sse_unrounded);

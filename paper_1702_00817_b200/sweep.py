@@ -143,7 +143,7 @@ def sweep_mse(t, stack: np.ndarray, r_min: int, r_max: int, device=None) -> np.n
     tr = resolve_transform(t)
     if transforms.is_proposed(tr) and _is_u8_exact(stack):
         x = torch.from_numpy(np.ascontiguousarray(stack.astype(np.uint8))).to(dev)
-        _, ssef = batch.sweep_retain_sse_unrounded(x, r_min, r_max)
+        _, ssef = batch.sweep_retain_sse_unrounded(x, r_min, r_max, rounded=False)
         torch.cuda.current_stream().synchronize()
         return ssef.cpu().numpy().astype(np.float64) / (4096.0 * h * w)
     x = torch.from_numpy(np.ascontiguousarray(stack)).to(dev)

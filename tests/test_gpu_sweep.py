@@ -72,6 +72,12 @@ def test_exact_sweep_unrounded_matches_golden(cuda):
         g = GOLDEN["config1"][name][str(r)]
         assert int(sse[0, r - 1]) == g["sse_rounded"]
         assert ssef[0, r - 1].item() / (4096.0 * IMAGES[name].size) == pytest.approx(g["mse_ref"], rel=1e-9)
+    none, only = batch.sweep_retain_sse_unrounded(x, 1, 45, rounded=False)  # the run_sweep form
+    assert none is None and torch.equal(only, ssef)
+    odd = torch.from_numpy(IMAGES["noise_64"][:, :56]).to(cuda)  # unpaired units
+    _, f1 = batch.sweep_retain_sse_unrounded(odd, 2, 9)
+    _, f2 = batch.sweep_retain_sse_unrounded(odd, 2, 9, rounded=False)
+    assert torch.equal(f1, f2)
 
 
 def test_run_sweep_matches_reference_semantics(cuda, tmp_path):

@@ -16,6 +16,7 @@ def timeit(fn, reps=20):
     return a.elapsed_time(b) / reps
 res["config1_sweep_rounded_ms"] = timeit(lambda: batch.sweep_retain_sse(x, 1, 45))
 res["config1_sweep_rounded_and_unrounded_ms"] = timeit(lambda: batch.sweep_retain_sse_unrounded(x, 1, 45))
+res["config1_sweep_unrounded_only_ms"] = timeit(lambda: batch.sweep_retain_sse_unrounded(x, 1, 45, rounded=False))
 res["config1_45_separate_retain_launches_ms"] = timeit(lambda: [batch.compress_retain(x, r, reconstruct=False) for r in range(1, 46)], 5)
 x0 = synth.config_images_device(0, [0], device=dev)
 res["config0_forward_int32_ms"] = timeit(lambda: batch.forward_int(x0))
