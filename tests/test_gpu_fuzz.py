@@ -79,3 +79,36 @@ def test_random_sweep_and_forward(cuda, case):
     torch.cuda.synchronize()
     assert np.array_equal(s.cpu().numpy(), exact.sweep_sse(host, r0, r1))
     assert np.array_equal(z.cpu().numpy().astype(np.int64), exact.forward_unscaled(host, level_shift=bool(case % 2)))
+
+
+def test_random_quant_all_tables_on_float_inverse(cuda):
+    """The float-pair-inverse kernel (k_quant_fi) for every table, not only
+    the coarse ones it runs by default (ADCT_FI_KERNEL=all; child process:
+    the switch is read once per process): the random quant cases again."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import numpy as np, torch, test_gpu_fuzz as F
+from oracle import exact
+from paper_1702_00817_b200 import batch, quant
+cuda = torch.device("cuda", 0)
+for case in range(F.CASES):
+    rng = np.random.default_rng(5000 + case)
+    x, host = F._batch(rng, cuda)
+    if case % 3 == 2:
+        qpu = rng.choice([1.0, 2.0, 2.5, 3.0, 7.49, 7.5, 16.0, 33.3, 100.0, 999.0, 8191.0, 9000.0], size=(8, 8))
+        qt = quant.quant_table(qprime_unrounded=qpu)
+    else:
+        qt = quant.quant_table(int(rng.integers(1, 101)))
+    want_rec, want_sse = exact.compress_quant(host, quant.qtab_qprime(qt))
+    rec, sse = batch.compress_quant(x, qt)
+    assert np.array_equal(rec.cpu().numpy(), want_rec) and np.array_equal(sse.cpu().numpy(), want_sse), case
+print("FI_ALL_OK")
+'''
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]),
+                                                        ADCT_FI_KERNEL="all"),
+                       capture_output=True, text=True, timeout=300, cwd=root)
+    assert "FI_ALL_OK" in r.stdout, r.stderr[-3000:]
