@@ -224,11 +224,12 @@ QParamsDev to_qparams_fi(const adct_qtab_t& t) {
 }
 
 // k_quant_fi is exact when every partial sum of the inverse, in units of
-// 1/64, stays below 2^24: they are bounded by sum_uv |W_uv| <=
-// sum_uv (|Z_uv| + Q'_uv / 2) E_uv <= 64 * 8192 + sum_uv qe_uv / 2
+// 1/64, stays below 2^24: they are bounded by sum_uv |W_uv| + 64 * 128.5
+// (the DC offset) <= sum_uv (|Z_uv| + Q'_uv / 2) E_uv + 8224
+// <= 64 * 8192 + 8224 + sum_uv qe_uv / 2
 // (|Z_uv| E_uv <= 128 n_u n_v * 64 / (n_u n_v) = 8192).
 bool fi_exact(const adct_qtab_t& t) {
-  double s = 64.0 * 8192.0;
+  double s = 64.0 * 8192.0 + 8224.0;
   for (int p = 0; p < 64; ++p) s += 0.5 * (double)t.qe[p];
   return s < 16777216.0;
 }
