@@ -1,7 +1,9 @@
 """the SSE exchange fused into the retain kernel epilogue.
 
 On one GPU the multi-peer push is exercised with several local vectors as
-the "peers" (no kernel waits on another), and the torch symmetric-memory
+the "peers" (no kernel waits on another), with another process's vector
+mapped through CUDA IPC (a second process's kernels store into the first
+process's memory; host synchronisation only), and the torch symmetric-memory
 wrapper (`shard.SseExchange`) at world size 1 in a child process.  Results
 must equal the C oracle's exact SSE (oracle/fast.py)."""
 
@@ -132,3 +134,73 @@ def test_quant_planes_exchange_on_local_peers(cuda, q, cr_w):
             assert torch.equal(v[offset:offset + 12], sse_ref.reshape(-1))
             assert bool((v[:offset] == -5).all()) and bool((v[offset + 12:] == -5).all())
         assert int(arrivals.abs().sum()) == 0
+
+
+_XPROC = r'''
+import sys, numpy as np, torch, torch.multiprocessing as mp
+from oracle import fast
+from paper_1702_00817_b200 import batch, quant, synth
+
+N, H, W, OFF = 6, 128, 512, 3
+
+
+def rank1(q_in, q_out):
+    """Another process: its images' SSE go into the parent's vector through
+    the CUDA-IPC mapping of that vector (the same kind of peer pointer torch
+    symmetric memory hands to the kernel); only the host synchronises."""
+    dev = torch.device("cuda", 0)
+    peer_vec = q_in.get()  # the parent's int64 vector, IPC-mapped into this process
+    own = torch.full_like(peer_vec, -9)
+    x = synth.images_device(range(100, 100 + N), H, W, 16, 8.0, 64.0, device=dev)
+    ptrs = torch.tensor([own.data_ptr(), peer_vec.data_ptr()], dtype=torch.int64, device=dev)
+    arrivals = torch.zeros(N, dtype=torch.int32, device=dev)
+    _, local = batch.compress_retain_exchange(x, 10, ptrs.data_ptr(), 2, OFF, arrivals)
+    planes = [x[:, :, :256].contiguous(), x[:, :64, 256:].contiguous()]
+    qt = quant.quant_table(10)
+    # quantised planes (push kernel after k_quant_fi): entries frame * 2 + plane
+    _, lq = batch.compress_quant_planes_exchange(planes, qt, ptrs.data_ptr(), 2, OFF + N,
+                                                 torch.zeros(2 * N, dtype=torch.int32, device=dev))
+    torch.cuda.synchronize()
+    q_out.put((local.cpu().numpy(), own.cpu().numpy(), lq.cpu().numpy(), x.cpu().numpy(),
+               [p.cpu().numpy() for p in planes]))
+    q_in.get()  # keep the mapping open until the parent has read its vector
+    del ptrs, own, peer_vec  # release the IPC mapping before the producer exits
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    ctx = mp.get_context("spawn")
+    q_in, q_out = ctx.Queue(), ctx.Queue()
+    vec = torch.full((OFF + 3 * N + 8,), -7, dtype=torch.int64, device="cuda:0")
+    p = ctx.Process(target=rank1, args=(q_in, q_out))
+    p.start()
+    q_in.put(vec)
+    local, own, lq, x, planes = q_out.get(timeout=240)
+    torch.cuda.synchronize()
+    got = vec.cpu().numpy()
+    q_in.put("done")
+    p.join(timeout=60)
+    _, want, _ = fast.compress_retain(x, 10)
+    # retain push: [OFF, OFF + N); planes push: [OFF + N, OFF + 3N) (frame * 2 + plane)
+    qp = quant.qtab_qprime(quant.quant_table(10))
+    wq = np.stack([fast.compress_quant(pl, qp)[1] for pl in planes], axis=1).reshape(-1)
+    assert np.array_equal(local, want) and np.array_equal(lq.reshape(-1), wq)
+    for v, fill in ((own, -9), (got, -7)):  # this process's vector and the other process's
+        assert np.array_equal(v[OFF:OFF + N], want), v
+        assert np.array_equal(v[OFF + N:OFF + 3 * N], wq), v
+        assert (v[:OFF] == fill).all() and (v[OFF + 3 * N:] == fill).all(), v
+    print("XPROC_OK")
+'''
+
+
+def test_exchange_into_another_process(cuda, tmp_path):
+    """The fused exchange across process boundaries: a second process's retain
+    kernel epilogue (and the push after its quant kernel) store into the first
+    process's SSE vector through a CUDA-IPC mapping.  Checked against the C
+    oracle.  One GPU, so the mapping is not NVLink P2P, but the pointer
+    handling is the same; no kernel waits on another (host sync only)."""
+    script = tmp_path / "xproc.py"
+    script.write_text(_XPROC)
+    r = subprocess.run([sys.executable, str(script)], env=dict(os.environ, PYTHONPATH=ROOT), capture_output=True,
+                       text=True, timeout=400, cwd=ROOT)
+    assert "XPROC_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
