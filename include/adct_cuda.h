@@ -159,7 +159,11 @@ int adct_compress_retain_exchange(const uint8_t* img, uint8_t* rec, int64_t n, i
  * K3 + K4 — fused quantised compression (single plane batch).
  * Level shift -128, forward T X T^T, quantise by Q' (round half away),
  * dequantise, inverse T^T D Y D T, +128, round, clamp; per-image SSE.
- * New (the reference has no quantised pipeline; BASELINE config 2). */
+ * New (the reference has no quantised pipeline; BASELINE config 2).
+ * Kernel choice is internal: tables whose reconstruction fits 16-bit lanes
+ * run the packed kernel; coarser ones (e.g. q = 10) the float-pair inverse;
+ * tables beyond both exactness bounds the 32-bit scalar kernel.  Results
+ * are identical (exact) either way. */
 int adct_compress_quant(const uint8_t* img, uint8_t* rec, int64_t n, int32_t h,
                         int32_t w, int64_t img_stride, int64_t rec_stride,
                         const adct_qtab_t* qtab, uint64_t* sse, void* stream);
