@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from ctypes import POINTER, c_double, c_float, c_int, c_int16, c_int32, c_int64, c_size_t, c_uint8, c_uint64, c_void_p
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_size_t, c_void_p
 
 from . import errors
 

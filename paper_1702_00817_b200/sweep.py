@@ -22,10 +22,9 @@ image, one r, PSNR per transform and optionally the reconstructions as PGM.
 from __future__ import annotations
 
 import json
-import math
 from dataclasses import asdict, dataclass
 from pathlib import Path
-from typing import Iterable, Sequence
+from typing import Sequence
 
 import numpy as np
 import torch

@@ -18,7 +18,6 @@ Generation is never inside a timed region.
 
 from __future__ import annotations
 
-import ctypes
 
 import numpy as np
 

@@ -5,7 +5,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1702_00817_b200.pipeline import HostPipeline, pin, unpin
-from paper_1702_00817_b200 import synth
+
 
 GB = 1 << 30
 h = torch.empty(GB, dtype=torch.uint8).pin_memory()
