@@ -141,11 +141,12 @@ def sweep_mse(t, stack: np.ndarray, r_min: int, r_max: int, device=None) -> np.n
     n, h, w = stack.shape
     tr = resolve_transform(t)
     if transforms.is_proposed(tr) and _is_u8_exact(stack):
-        x = torch.from_numpy(np.ascontiguousarray(stack.astype(np.uint8))).to(dev)
+        u8 = stack if stack.dtype == np.uint8 else stack.astype(np.uint8)
+        x = codec._host_tensor(u8).to(dev)
         _, ssef = batch.sweep_retain_sse_unrounded(x, r_min, r_max, rounded=False)
         torch.cuda.current_stream().synchronize()
         return ssef.cpu().numpy().astype(np.float64) / (4096.0 * h * w)
-    x = torch.from_numpy(np.ascontiguousarray(stack)).to(dev)
+    x = codec._host_tensor(stack).to(dev)
     if x.dtype != torch.uint8:
         x = x.to(torch.float64)
     sse = batch.sweep_dense_sse(x, np.asarray(tr.matrix, dtype=np.float64), r_min, r_max)
@@ -153,31 +154,68 @@ def sweep_mse(t, stack: np.ndarray, r_min: int, r_max: int, device=None) -> np.n
     return sse.cpu().numpy() / float(h * w)
 
 
+def _batch_of(images, idx) -> np.ndarray:
+    """(N, H, W) batch of images[idx]: a zero-copy view when they are
+    consecutive C-contiguous planes of one allocation (a corpus loaded as one
+    batch, pgm.load_batch, synth.images_np), else one stacked copy."""
+    arrs = [np.asarray(images[k][1]) for k in idx]
+    a0 = arrs[0]
+    owner = a0.base
+    if owner is not None and all(a.base is owner and a.flags.c_contiguous and a.dtype == a0.dtype
+                                 and a.shape == a0.shape for a in arrs):
+        plane = a0.nbytes
+        p0 = a0.__array_interface__["data"][0]
+        if all(a.__array_interface__["data"][0] == p0 + k * plane for k, a in enumerate(arrs)):
+            # every plane lies inside `owner`, back to back: one strided view covers them
+            return np.lib.stride_tricks.as_strided(a0, shape=(len(arrs),) + a0.shape,
+                                                   strides=(plane,) + a0.strides, writeable=False)
+    return np.stack(arrs)
+
+
 def run_sweep(config: ExperimentConfig, images: Sequence[tuple[str, np.ndarray]] | None = None):
     """(records, summaries, ape) exactly as cli.run_sweep (cli.py:87-124) returns them.
 
     `images` are (image_id, samples) pairs; None loads them like the
-    reference (load_corpus_images: config.corpus_path or the synthesizer)."""
+    reference (load_corpus_images: config.corpus_path or the synthesizer).
+    One batched sweep per (transform, image shape).  The summaries come
+    straight from the MSE matrix, with the reference's own float64 averages
+    (metrics.summarize, metrics.py:75-97: np.mean over the images in order).
+    Transforms sharing a name merge their groups as the reference does, and
+    then go through metrics.summarize itself."""
     if images is None:
         images = load_corpus_images(config)
     records: list[metrics.QualityRecord] = []
     groups = _group_by_shape(images)
-    for t in config.transforms:
-        name = _name(t)
-        per_image: dict[int, np.ndarray] = {}
-        for _, idx in groups.items():
-            stack = np.stack([np.asarray(images[k][1]) for k in idx])
-            m = sweep_mse(t, stack, config.r_min, config.r_max)
-            for row, k in enumerate(idx):
-                per_image[k] = m[row]
+    batches = {key: _batch_of(images, idx) for key, idx in groups.items()}
+    r_values = list(config.r_values)
+    names = [_name(t) for t in config.transforms]
+    per_name: dict[str, tuple[np.ndarray, np.ndarray]] = {}
+    for t, name in zip(config.transforms, names):
+        m = np.empty((len(images), len(r_values)), dtype=np.float64)
+        for key, idx in groups.items():
+            m[idx] = sweep_mse(t, batches[key], config.r_min, config.r_max)
+        p = np.empty_like(m)
         for k, (image_id, _) in enumerate(images):
-            for j, r in enumerate(config.r_values):
-                err = float(per_image[k][j])
-                records.append(metrics.QualityRecord(image_id, name, r, err, metrics.psnr(err)))
-    summaries = metrics.summarize(records, psnr_from_avg_mse=config.psnr_from_avg_mse)
+            for j, r in enumerate(r_values):
+                err = float(m[k, j])
+                p[k, j] = metrics.psnr(err)  # math.log10, as the reference's per-record psnr
+                records.append(metrics.QualityRecord(image_id, name, r, err, float(p[k, j])))
+        per_name[name] = (m, p)
+    if images and len(set(names)) == len(names):
+        summaries = []
+        for name in sorted(names):
+            m, p = per_name[name]
+            avg_m = np.ascontiguousarray(m.T).mean(axis=1)  # per r, over the images in order
+            avg_p = np.ascontiguousarray(p.T).mean(axis=1)
+            for j, r in enumerate(r_values):
+                am = float(avg_m[j])
+                ap = metrics.psnr(am) if config.psnr_from_avg_mse else float(avg_p[j])
+                summaries.append(metrics.CorpusSummary(name, r, am, ap, len(images)))
+    else:
+        summaries = metrics.summarize(records, psnr_from_avg_mse=config.psnr_from_avg_mse)
     avg_mse = {(s.transform_name, s.r): s.avg_mse for s in summaries}
     ape = {}
-    if "dct" in [_name(t) for t in config.transforms]:
+    if "dct" in names:
         for s in summaries:
             ref = avg_mse[("dct", s.r)]
             ape[(s.transform_name, s.r)] = metrics.ape_vs_dct(s.avg_mse, ref) if ref > 0 else float("nan")
