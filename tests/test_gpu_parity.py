@@ -267,3 +267,22 @@ print("ALT_OK")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PYTHONPATH=root, **env),
                        capture_output=True, text=True, timeout=300)
     assert "ALT_OK" in r.stdout, r.stderr[-3000:]
+
+
+def test_float_inverse_at_its_acceptance_limit(cuda):
+    """Custom tables whose sum(Q'E) sits just under k_quant_fi's exactness
+    bound (capi.cu fi_exact; the same tables tests/test_fi_model.py checks in
+    a float32 model): the kernel on adversarial blocks equals the oracle."""
+    rng = np.random.default_rng(99)
+    budget = 2 * (2.0**24 - 64 * 8192 - 8224) - 1
+    checker = ((np.indices((8, 8)).sum(axis=0) % 2) * 255).astype(np.uint8)
+    for _ in range(4):
+        w = rng.random((8, 8))
+        qp = np.maximum(1, np.floor(budget * w / w.sum() / exact.E)).astype(np.int64)
+        qt = quant.quant_table(qprime_unrounded=qp.astype(np.float64))
+        assert np.array_equal(quant.qtab_qprime(qt), qp)
+        x = np.concatenate([np.tile(checker, (2, 4)), (rng.integers(0, 2, (16, 32)) * 255).astype(np.uint8),
+                            rng.integers(0, 256, (16, 32)).astype(np.uint8)])[None]
+        rec, sse = batch.compress_quant(torch.from_numpy(x).to(cuda), qt)
+        wr, ws = exact.compress_quant(x, qp)
+        assert np.array_equal(rec.cpu().numpy(), wr) and np.array_equal(sse.cpu().numpy(), ws)
