@@ -817,6 +817,14 @@ __host__ __device__ constexpr SweepTables make_sweep_tables() {
 }
 __constant__ SweepTables c_sweep = make_sweep_tables();
 
+// PRMT with sign replication (selector nibble msb set: the byte's sign fills
+// it); the __byte_perm intrinsic ignores that bit, so this is inline PTX.
+__device__ __forceinline__ u32 prmt_sext(u32 a, u32 sel) {
+  u32 r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(a), "r"(sel));
+  return r;
+}
+
 template <bool PAIR, bool FSSE = false>
 __global__ void __launch_bounds__(kSweepThreads)
     k_sweep_inc(PlaneSetDev ps, int r_min, int r_max, u64* __restrict__ sse, u64* __restrict__ ssef = nullptr) {
@@ -915,14 +923,22 @@ __global__ void __launch_bounds__(kSweepThreads)
                                __byte_perm(p23, 0u, 0x4240), __byte_perm(p23, 0u, 0x4341),
                                __byte_perm(p45, 0u, 0x4240), __byte_perm(p45, 0u, 0x4341),
                                __byte_perm(p67, 0u, 0x4240), __byte_perm(p67, 0u, 0x4341)};
+            // per lane d = 64 x - clamp(64 x_hat) (|d| <= 16320, linear form);
+            // a row's 16 squares stay below 2^32 (16 * 16320^2), so they add up
+            // in 32 bits; lanes split by sign-extending PRMTs
+            u32 row = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const u32 c = __vmaxu2(__vminu2(U[i][j], 0x9FE09FE0u), 0x60206020u);
               const u32 d = (xr[j] << 6) + 0x60206020u - c;
-              const int da = (int)(d << 16) >> 16;
-              const int db = (int)(d - (u32)da) >> 16;
-              accf += (u64)(da * da) + (PAIR ? (u64)(db * db) : 0ull);
+              const u32 da = prmt_sext(d, 0x9910);  // lane A, sign-extended
+              row += da * da;
+              if (PAIR) {
+                const u32 db = prmt_sext(d - da, 0xBB32);  // lane B (A's borrow removed)
+                row += db * db;
+              }
             }
+            accf += row;
           }
         }
       }
