@@ -279,7 +279,10 @@ typedef struct adct_pipeline adct_pipeline_t;
 
 int adct_pipeline_create(int32_t device, size_t chunk_bytes, adct_pipeline_t** out);
 int adct_pipeline_destroy(adct_pipeline_t* p);
-/* host_rec nullable; host_sse: host uint64 [n].  Blocks until done. */
+/* host_rec nullable; host_sse: host uint64 [n].  Blocks until done.
+ * Calls on one pipeline from several threads are serialised (a pipeline is
+ * one set of streams and staging slots); use one pipeline per thread for
+ * concurrent transfers. */
 int adct_pipeline_compress_retain(adct_pipeline_t* p, const uint8_t* host_img,
                                   uint8_t* host_rec, int64_t n, int32_t h, int32_t w,
                                   int32_t r, uint64_t* host_sse);

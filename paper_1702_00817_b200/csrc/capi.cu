@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -1009,6 +1010,7 @@ struct adct_pipeline {
   uint64_t* d_sse = nullptr;  // SSE of a whole call, copied to the host once at the end
   int64_t sse_cap = 0;
   adct::HostCopyPool* pool = nullptr;  // host threads for the staging memcpys
+  std::mutex mu;  // calls on one pipeline are serialised (one set of streams and staging slots)
 };
 
 namespace {
@@ -1312,18 +1314,24 @@ int adct_pipeline_destroy(adct_pipeline_t* p) {
 
 int adct_pipeline_compress_retain(adct_pipeline_t* p, const uint8_t* host_img, uint8_t* host_rec,
                                   int64_t n, int32_t h, int32_t w, int32_t r, uint64_t* host_sse) {
+  if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(p->mu);
   return pipeline_run(p, host_img, host_rec, n, h, w, 0, r, nullptr, host_sse);
 }
 
 int adct_pipeline_compress_quant(adct_pipeline_t* p, const uint8_t* host_img, uint8_t* host_rec,
                                  int64_t n, int32_t h, int32_t w, const adct_qtab_t* qtab,
                                  uint64_t* host_sse) {
+  if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(p->mu);
   return pipeline_run(p, host_img, host_rec, n, h, w, 1, 0, qtab, host_sse);
 }
 
 int adct_pipeline_compress_quant_planes(adct_pipeline_t* p, const adct_plane_t* host_planes,
                                         int32_t n_planes, int64_t n_frames, const adct_qtab_t* qtab,
                                         uint64_t* host_sse) {
+  if (p == nullptr) return ADCT_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(p->mu);
   return pipeline_frames_run(p, host_planes, n_planes, n_frames, 1, 0, qtab, host_sse);
 }
 

@@ -353,3 +353,36 @@ def test_forward_unscaled_device_tensors(cuda):
     fb = rng.normal(0, 50, (4, 8, 8))
     zf = codec.forward_2d_unscaled(T, torch.as_tensor(fb, device=cuda))
     assert np.abs(zf.cpu().numpy() - exact.T @ fb @ exact.T.T).max() < 1e-9
+
+
+def test_host_pipeline_shared_by_threads(cuda):
+    """Several Python threads on ONE HostPipeline (ctypes releases the GIL):
+    the library serialises the calls, every result is exact."""
+    import threading
+
+    imgs = synth.images_np(range(60, 66), 128, 256, 16, 8.0, 64.0)
+    want_rec, want_sse, _ = exact.compress_retain(imgs, 7)
+    qt = quant.quant_table(30)
+    wq, wqs = exact.compress_quant(imgs, quant.qtab_qprime(qt))
+    errors = []
+    with HostPipeline(0, chunk_bytes=1 << 16) as p:
+        def work(k):
+            try:
+                for _ in range(3):
+                    rec = np.empty_like(imgs)
+                    if k % 2:
+                        _, s = p.compress_retain(imgs, 7, rec)
+                        ok = np.array_equal(rec, want_rec) and np.array_equal(s, want_sse)
+                    else:
+                        _, s = p.compress_quant(imgs, qt, rec)
+                        ok = np.array_equal(rec, wq) and np.array_equal(s, wqs)
+                    if not ok:
+                        errors.append(k)
+            except Exception as exc:  # noqa: BLE001
+                errors.append(repr(exc))
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    assert not errors, errors
