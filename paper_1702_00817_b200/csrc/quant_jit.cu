@@ -179,7 +179,7 @@ CUfunction build(int kind, const QParamsDev& q) {
   const char* expr = kernel_expression(kind);
   CUfunction fn = nullptr;
   bool good = expr != nullptr && nv.add_name(prog, expr) == 0;
-  // ADCT_JIT_OPTS: one extra NVRTC option (e.g. -DADCT_QP_FOLD=0) for A/B runs
+  // ADCT_JIT_OPTS: one extra NVRTC option (e.g. --maxrregcount=120) for A/B runs
   const char* extra = std::getenv("ADCT_JIT_OPTS");
   if (extra != nullptr && *extra == '\0') extra = nullptr;  // set but empty: no extra option
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", extra ? extra : ""};
