@@ -494,7 +494,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // ---------------------------------------------------------------------------
 // K3f k_quant_fi: the float-pair inverse.  Any table (q = 10's reconstruction
-// needs 17 bits, beyond the packed kernels' 16-bit lanes).  The forward and
+// needs 17 bits, beyond the packed kernels' 16-bit lanes).  Same pipeline as
+// K3: forward_2d_unscaled of the level-shifted block, the D^2-folded
+// quantiser, inverse_2d (reference codec.py:74-104, 84-87), round, clamp, SSE.  The forward and
 // the float quantiser run packed as in k_quant_p; from the quantised integers
 // on, the two blocks travel as fp32 pairs (A, B) in 64-bit register pairs, so
 // every step of the inverse is one FP32x2 instruction for both blocks on the
