@@ -250,3 +250,32 @@ def test_csv_writers_match_reference(reference):
         reference.metrics.write_summary_csv(b, ref)
         assert a.getvalue() == b.getvalue()
     assert metrics.format_float(float("inf")) == reference.metrics.format_float(float("inf")) == "inf"
+
+
+def test_missing_native_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libadct_cuda.so every compute entry point
+    raises NativeLibraryError (child process: the path is read at import)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import numpy as np, torch
+from paper_1702_00817_b200 import _lib, batch, codec, quant, transforms
+for call in (lambda: _lib.lib(),
+             lambda: quant.quant_table(50),
+             lambda: batch.compress_retain(torch.zeros((1, 8, 8), dtype=torch.uint8), 10),
+             lambda: codec.compress_image(transforms.proposed_transform(), np.zeros((8, 8)), 10)):
+    try:
+        call()
+    except (_lib.NativeLibraryError, RuntimeError, ValueError) as exc:
+        msg = str(exc)
+        assert "not found" in msg or "CUDA" in msg or "GPU" in msg or "no CPU path" in msg, exc
+    else:
+        raise SystemExit("a call succeeded without the native library")
+print("LOUD_OK")
+'''
+    env = dict(os.environ, PYTHONPATH=root, ADCT_LIB_PATH=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env)
+    assert "LOUD_OK" in r.stdout, r.stderr[-2000:]
