@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(kSweepThreads)
     }
   }
   const int nr = r_max - r_min + 1;
+  const u32 four = 4u | ((u32)r_min >> 8);  // 4 (r_min <= 64), opaque to the compiler: stays an IMAD
   u64* out = sse != nullptr ? sse + L.frame * nr : nullptr;
 #pragma unroll 1
   for (int r = 1; r <= r_max; ++r) {
@@ -894,10 +895,13 @@ __global__ void __launch_bounds__(kSweepThreads)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           if (!FSSE) {
-            const u32 q[4] = {__byte_perm(clamp_shift<true>(U[i][0]), clamp_shift<true>(U[i][1]), 0x7531),
-                              __byte_perm(clamp_shift<true>(U[i][2]), clamp_shift<true>(U[i][3]), 0x7531),
-                              __byte_perm(clamp_shift<true>(U[i][4]), clamp_shift<true>(U[i][5]), 0x7531),
-                              __byte_perm(clamp_shift<true>(U[i][6]), clamp_shift<true>(U[i][7]), 0x7531)};
+            // clamp on the ALU, the x4 (moving bits 6..13 to bytes 1/3) as a
+            // multiply by a run-time 4 on the otherwise idle FMA pipe
+            u32 cs[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cs[j] = __vmaxu2(__vminu2(U[i][j], 0x9FFF9FFFu), 0x60006000u) * four;
+            const u32 q[4] = {__byte_perm(cs[0], cs[1], 0x7531), __byte_perm(cs[2], cs[3], 0x7531),
+                              __byte_perm(cs[4], cs[5], 0x7531), __byte_perm(cs[6], cs[7], 0x7531)};
             const u32 ow[4] = {w[i].x, w[i].y, w[i].z, w[i].w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
