@@ -72,3 +72,36 @@ def test_two_rank_plan_config4_frames_and_weak_option():
     assert d["config"]["pixels_per_step"] == 512 * (3840 * 2160 + 2 * 1920 * 1080)
     w = _plan(2, "--scaling", "weak")
     assert w["config"]["units_per_gpu"] == 4096 and w["config"]["pixels_per_step"] == 2 * 17179869184
+
+
+def test_clock_sampler_parses_nvidia_smi_lines():
+    """The clocks record of the bench line: median SM clock under load, max,
+    and every throttle reason seen, from nvidia-smi's CSV samples."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    cs = bench.ClockSampler(0)
+    cs.proc = type("P", (), {"terminate": lambda self: None, "wait": lambda self, timeout=None: 0,
+                             "kill": lambda self: None})()
+    cs.t = type("T", (), {"join": lambda self, timeout=None: None})()
+    cs.lines = [
+        "0, 1965, 1965, 900.1, 0x0, Not Active, Not Active, Not Active, Not Active",
+        "0, 1800, 1965, 1000.3, 0x4, Not Active, Not Active, Not Active, Active",
+        "0, 1965, 1965, 950.0, 0x0, Not Active, Not Active, Not Active, Not Active",
+        "garbage line",
+    ]
+    rec = cs.stop()
+    assert rec["sm_mhz"] == 1965.0 and rec["sm_max_mhz"] == 1965.0 and rec["samples"] == 3
+    assert rec["reasons"] == ["sw_power_cap"]
+
+
+def test_hbm_peak_source(tmp_path, monkeypatch):
+    sys.path.insert(0, ROOT)
+    import bench
+
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    peak, src = bench.measured_hbm_peak()
+    assert peak == bench.FALLBACK_HBM_GBS and "fallback" in src
+    (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps({"hbm_gbs": 6462.7}))
+    peak, src = bench.measured_hbm_peak()
+    assert peak == 6462.7 and "MEASURED_PEAKS" in src
