@@ -7,7 +7,9 @@ through its own page-locked ring, filled and drained by host threads while
 the copies run (never registered per call); page-locked arrays
 (`pinned_empty`, or `pin()` for repeated use) are copied directly.
 `register=True` page-locks the caller's arrays for the call instead
-(arrays that are already pinned are left alone).
+(arrays that are already pinned are left alone; not for arrays that other
+threads are passing to concurrent calls at the same time — use `pin()` once).
+Several threads may share one pipeline: the library serialises its calls.
 """
 
 from __future__ import annotations
